@@ -37,6 +37,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 
 #define ISMG_B200_ABI_VERSION 1
 
@@ -272,6 +275,9 @@ int ismg_state_download(const ismg_state* st, double* u, size_t u_count, double*
 int ismg_step(ismg_state* st, ismg_solver* s, ismg_report* rep, ismg_step_metrics* current,
               int64_t fine_cells);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

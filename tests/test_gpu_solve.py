@@ -1,0 +1,136 @@
+"""GPU parity, solve and projection-step level (north star: identical
+iteration counts, fields within 1e-10 relative L2 in fp64).
+
+The reference answers come from the committed golden vectors (produced by the
+unmodified reference) and from the C oracle run in the same process.
+"""
+import numpy as np
+import pytest
+
+from cases import a3_rhs, cavity, golden_grids, random_field, torus, with_side
+from paper_1309_7128_b200.api import (BoundaryCondition, CycleConfig, FluidState, RunMetrics, ScalarField, Scheme,
+                                      Side, setup_channel_jets, setup_jet, setup_lid_cavity)
+
+pytestmark = pytest.mark.gpu
+REL_L2 = 1e-10  # BASELINE.json north_star tolerance
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import paper_1309_7128_b200 as P
+    if P.device_count() < 1:
+        pytest.skip("no GPU")
+    return P
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+@pytest.mark.parametrize("name,g", golden_grids(), ids=[n for n, _ in golden_grids()])
+def test_solves_match_golden(dev, golden, name, g):
+    P, z = dev, golden
+    bb = ScalarField(g.nx, g.ny, z[name + "/b"].copy())
+    bb.shift_interior(-bb.interior_mean())
+    for s in Scheme:
+        key = "%s/solve_%d" % (name, int(s))
+        if key + "/x" not in z and key + "/error" not in z:
+            continue
+        cfg = CycleConfig(scheme=s, tile=g.tile, depth=3, tol_fine=1e-9, tol_coarse=1e-8, max_total_sweeps=4000)
+        if key + "/error" in z:
+            from paper_1309_7128_b200._lib import IsmgError
+            with pytest.raises(IsmgError) as e:
+                solver = P.PressureSolver(g, cfg)
+                solver.solve(ScalarField(g.nx, g.ny), bb, RunMetrics(g.nx * g.ny))
+            assert e.value.code == z[key + "/error"][0]
+            continue
+        solver = P.PressureSolver(g, cfg)
+        m = RunMetrics(g.nx * g.ny)
+        x = ScalarField(g.nx, g.ny)
+        rep = solver.solve(x, bb, m)
+        counts = [int(rep.converged), rep.fine_sweeps, rep.coarse_sweeps, m.current.restrictions,
+                  m.current.prolongations]
+        assert counts == z[key + "/counts"].tolist(), (s, counts)
+        assert rel_l2(x.interior(), ScalarField(g.nx, g.ny, z[key + "/x"]).interior()) <= REL_L2
+        assert m.current.lap_equiv == z[key + "/scalars"][1]
+
+
+def golden_runs():
+    c1 = setup_lid_cavity(32, 100.0)
+    c1.dt = 100.0 / 32
+    return [("lid32", c1, CycleConfig(tile=8), 25), ("jet32x64", setup_jet(32, 64, 0.1, 8), CycleConfig(tile=8), 12),
+            ("chan24x48", setup_channel_jets(24, 48, 0.1, 6), CycleConfig(tile=8), 8)]
+
+
+@pytest.mark.parametrize("name,case,cfg,nsteps", golden_runs(), ids=[r[0] for r in golden_runs()])
+def test_projection_runs_match_golden(dev, golden, name, case, cfg, nsteps):
+    P = dev
+    case.steps = nsteps
+    case.t_max = 0.0
+    case.steady_tol = 0.0
+    res = P.run_case(case, cfg)
+    rows = [[r.step, r.fine_sweeps, r.coarse_sweeps, r.sync_fine, r.sync_coarse, r.restrictions, r.prolongations,
+             int(r.converged)] for r in res.metrics.rows]
+    assert rows == golden["run/%s/rows" % name].tolist()
+    st = res.state
+    assert rel_l2(st.vel.u_data, golden["run/%s/u" % name]) <= REL_L2
+    assert rel_l2(st.vel.v_data, golden["run/%s/v" % name]) <= REL_L2
+    assert rel_l2(st.p.data, golden["run/%s/p" % name]) <= REL_L2
+
+
+def test_lid256_config1_counts_and_fields(dev, port):
+    """BASELINE config 1 (lid 256^2, Re 100, tile 16, dt = Re/n) for 60 steps."""
+    P = dev
+    case = setup_lid_cavity(256, 100.0)
+    case.dt, case.steps, case.t_max, case.steady_tol = 100.0 / 256, 60, 0.0, 0.0
+    cfg = CycleConfig(tile=16)
+    res = P.run_case(case, cfg)
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, _ = port.run_steps(case.grid, cfg, st, 60)
+    got = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in res.metrics.rows]
+    want = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in rows]
+    assert got == want
+    assert rel_l2(res.state.vel.u_data, st.vel.u_data) <= REL_L2
+    assert rel_l2(res.state.vel.v_data, st.vel.v_data) <= REL_L2
+    assert rel_l2(res.state.p.data, st.p.data) <= REL_L2
+
+
+def test_a3_four_schemes_agree(dev):
+    """acceptance.cpp:173-248 (A3) on the GPU."""
+    P = dev
+    b = a3_rhs(64)
+    g = cavity(64, 64)
+    sols = []
+    for s, size in ((Scheme.plain_gs, 0), (Scheme.ismg, 8), (Scheme.gmg, 8), (Scheme.acm, 4)):
+        cfg = CycleConfig(scheme=s, tol_fine=1e-7, tol_coarse=1e-7)
+        if s == Scheme.acm:
+            cfg.depth = size
+        elif s != Scheme.plain_gs:
+            cfg.tile = size
+        x = ScalarField(64, 64)
+        rep = P.PressureSolver(g, cfg).solve(x, b, RunMetrics(64 * 64))
+        assert rep.converged
+        x.shift_interior(-x.interior_mean())
+        sols.append(x.interior().copy())
+    worst = max(np.abs(sols[a] - sols[c]).max() for a in range(4) for c in range(a + 1, 4))
+    assert worst < 1e-5
+
+
+def test_zero_rhs_and_budget(dev):
+    """test_cycles.cpp:75-93 and :268-291 on the device path."""
+    P = dev
+    g = cavity(16, 16)
+    for s in Scheme:
+        rep = P.PressureSolver(g, CycleConfig(scheme=s, tile=4, depth=3)).solve(
+            ScalarField(16, 16), ScalarField(16, 16), RunMetrics(256))
+        assert rep.converged and rep.fine_sweeps == 0 and rep.coarse_sweeps == 0 and rep.residual == 0.0
+    rng = np.random.default_rng(11)
+    b = random_field(32, 32, rng)
+    b.shift_interior(-b.interior_mean())
+    for s in (Scheme.plain_gs, Scheme.ismg, Scheme.acm):
+        cfg = CycleConfig(scheme=s, tile=8, depth=3, tol_fine=1e-12, tol_coarse=1e-12, max_total_sweeps=3)
+        rep = P.PressureSolver(cavity(32, 32), cfg).solve(ScalarField(32, 32), b, RunMetrics(1024))
+        assert not rep.converged and rep.fine_sweeps + rep.coarse_sweeps <= 3
