@@ -242,6 +242,11 @@ int ismg_solve_host(ismg_solver* s, double* x_host, const double* b_host, size_t
                     ismg_report* rep, ismg_step_metrics* current, int64_t fine_cells);
 /* stats of the last solve on this solver */
 int ismg_solver_last_stats(const ismg_solver* s, ismg_solve_stats* out);
+/* Coarse-visit log of the last solve: per outer iteration (restriction) the
+ * number of coarse sweeps and of fine sweeps that followed, interleaved
+ * (c0, f0, c1, f1, ...). *n receives the number of visits; at most cap visits
+ * are written (out may be NULL to query). */
+int ismg_solver_visit_log(const ismg_solver* s, int32_t* out, size_t cap, size_t* n);
 
 /* ---- projection step ------------------------------------------------------ */
 /* apply_scalar_bc — field.hpp:77-96 */

@@ -388,6 +388,17 @@ int ismg_solve_host(ismg_solver* s, double* x_host, const double* b_host, size_t
     });
 }
 
+int ismg_solver_visit_log(const ismg_solver* s, int32_t* out, size_t cap, size_t* n) {
+    return guard([&] {
+        need(s, "solver");
+        need(n, "n");
+        const std::vector<int>& log = s->impl.visit_log;
+        *n = log.size() / 2;
+        if (out)
+            for (size_t k = 0; k < std::min(cap, *n) * 2; ++k) out[k] = log[k];
+    });
+}
+
 int ismg_solver_last_stats(const ismg_solver* s, ismg_solve_stats* out) {
     return guard([&] {
         need(s, "solver");

@@ -1,0 +1,404 @@
+// fused.cu — the hot path: device-resident solve_two_level (cycles.hpp:101-165).
+//
+// One fine iteration = ONE HBM pass (24 B/cell: read x, b; write x):
+//   x' = x + c (pending anchor, smoother.hpp:145-148)  -> red half-sweep ->
+//   black half-sweep (smoother.hpp:101-117) -> residual (smoother.hpp:121-141)
+//   -> 16h/32h tile sums of the residual (restrict_sum, coarsening.hpp:471-480)
+//   -> sum of x (next anchor) and max|r|.
+// Rows are streamed through a shared-memory ring by TMA bulk copies
+// (cp.async.bulk + mbarrier); each CTA owns a 256-column strip x H-row chunk
+// and recomputes a 3-cell halo, so the red, black and residual stages run in
+// one pass with 2 CTA barriers per row. Each thread owns a column pair and
+// keeps its vertical window in registers; horizontal neighbours come from
+// shared memory. A tile row of 32 (16) cells maps to 16 (8) lanes whose
+// partial sums are folded by warp shuffles.
+//
+// Control flow never leaves the device: the last CTA of every kernel applies
+// the reference's branch logic to the reduced scalars and writes the next
+// phase into a device state block. The host replays a CUDA graph of
+// [coarse-visit, fine-pass] slots; kernels whose phase is not current exit at
+// once. The host only polls the phase once per graph launch.
+#include "fused_impl.cuh"
+
+namespace ismgb {
+namespace fz {
+
+// ---- per-CTA epilogue + control flow (last CTA) ------------------------------
+__device__ void fine_decide(const Params& P, int mode, double r, double sum, int nan) {
+    Ctl* s = P.ctl;
+    if (nan) s->nan_seen = 1;
+    s->passes += 1;
+    s->r = r;
+    if (P.singular) {  // anchor after every residual check (field.hpp:49,53-59)
+        s->shift = -(sum / P.ncells);
+        s->has_shift = 1;
+    }
+    if (mode != kResid) s->cur ^= 1;
+    auto to_coarse = [&]() {
+        s->restrictions += 1;
+        if (s->nvisits < P.visit_cap) {
+            P.visit_log[2 * s->nvisits] = 0;
+            P.visit_log[2 * s->nvisits + 1] = 0;
+        }
+        s->nvisits += 1;
+        s->phase = kCoarse;
+    };
+    if (mode == kFine) {  // cycles.hpp:147-161
+        s->total += 1;
+        s->fine += 1;
+        if (s->nvisits > 0 && s->nvisits <= P.visit_cap) P.visit_log[2 * (s->nvisits - 1) + 1] += 1;
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else if (s->total >= P.max_total) {
+            s->phase = kDone, s->converged = 0;
+        } else if (r > P.stall * s->prev) {
+            to_coarse();
+        } else {
+            s->prev = r;
+            s->phase = kFine;
+        }
+    } else if (mode == kProlong) {  // cycles.hpp:138-146
+        s->prolongations += 1;
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else {
+            s->prev = r;
+            if (s->total >= P.max_total) s->phase = kDone, s->converged = 0;
+            else s->phase = kFine;
+        }
+    } else {  // initial residual, cycles.hpp:111-118
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else if (s->total >= P.max_total) {
+            s->phase = kDone, s->converged = 0;
+        } else {
+            to_coarse();
+        }
+    }
+}
+
+__device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, int nan) {
+    const int nb = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    double bm = block_max(mx, sm.red[0]);
+    double bs = block_sum(sx, sm.red[1]);
+    int anynan = __syncthreads_or(nan);
+    if (threadIdx.x == 0) {
+        P.part[2 * bid] = bm;
+        P.part[2 * bid + 1] = bs;
+        if (anynan) P.ctl->nan_seen = 1;
+        __threadfence();
+        const unsigned t = atomicAdd(P.ticket, 1u);
+        sm.last = (t == unsigned(nb - 1));
+    }
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    double m = 0.0, s = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        m = fmax(m, __ldcg(&P.part[2 * k]));
+        s += __ldcg(&P.part[2 * k + 1]);
+    }
+    m = block_max(m, sm.red[0]);
+    s = block_sum(s, sm.red[1]);
+    if (threadIdx.x == 0) {
+        fine_decide(P, mode, m, s, 0);
+        *P.ticket = 0u;
+        __threadfence();
+    }
+}
+
+// ---- SWEEP body: anchor-shift, red, black, residual, restriction ------------
+__device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
+    const int a = blockIdx.x * kW;
+    const int r0 = blockIdx.y * P.H, r1 = min(r0 + P.H, P.ny);
+    const double* xin = st.buf[st.cur];
+    double* xout = st.buf[st.cur ^ 1];
+    const double* b = st.b;
+    const bool shift_on = st.has_shift != 0;
+    const double c = st.shift;
+
+    const int t = threadIdx.x;
+    const bool owned = t < kPairs;
+    const bool halo = (t == kPairs) || (t == kPairs + 1);
+    const bool active = owned || halo;
+    const int c0 = owned ? a + 2 * t : (t == kPairs ? a - 2 : a + kW);
+    const int sidx = c0 - (a - 4);
+    const bool in0 = active && c0 >= 0 && c0 < P.nx, in1 = active && c0 + 1 >= 0 && c0 + 1 < P.nx;
+    const bool inL = active && c0 - 1 >= 0 && c0 - 1 < P.nx, inR = active && c0 + 2 < P.nx && c0 + 2 >= 0;
+    const double dc0 = col_diag(P, c0), dc1 = col_diag(P, c0 + 1);
+    const uint32_t ncopy = uint32_t(((min(a + kW + 4, P.nx + 5) - (a - 4)) + 1) & ~1);
+
+    if (t == 0) {
+        for (int s = 0; s < kRing; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int kfirst = r0 - 3, klast = r1 + 2;
+    if (t == 0)
+        for (int k = kfirst; k <= min(klast, kfirst + kAheadSweep - 1); ++k) issue_row(sm, P, xin, b, k, a, ncopy);
+
+    // vertical register window: x{d} = row k-d of this thread's column pair
+    double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, x3a = 0, x3b = 0, x4a = 0, x4b = 0;
+    double b0a = 0, b0b = 0, b1a = 0, b1b = 0, b2a = 0, b2b = 0, b3a = 0, b3b = 0;
+    double mx = 0.0, sx = 0.0, tacc = 0.0;
+    int nan = 0;
+    const int g = P.tile >> 1;
+
+    for (int k = kfirst; k <= klast; ++k) {
+        const int slot = (k + 2 * kRing) % kRing;
+        const uint32_t parity = uint32_t(((k - kfirst) / kRing) & 1);
+        // -- load row k (raw + pending anchor shift), masked outside the domain
+        mbar_wait(&sm.bar[slot], parity);
+        const bool rk = k >= 0 && k < P.ny;
+        if (active) {
+            const double2 xv = *reinterpret_cast<const double2*>(&sm.x[slot][sidx]);
+            const double2 bv = *reinterpret_cast<const double2*>(&sm.b[slot][sidx]);
+            x0a = (rk && in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
+            x0b = (rk && in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
+            b0a = bv.x;
+            b0b = bv.y;
+        }
+        // -- stage 1: red half-sweep of row j = k-1
+        {
+            const int j = k - 1;
+            if (active && j >= r0 - 2 && j >= 0 && j < P.ny) {
+                const int js = (j + 2 * kRing) % kRing;
+                const double dr = row_diag(P, j);
+                if ((j & 1) == 0) {  // red cell is c0
+                    if (in0) {
+                        double W = 0.0;
+                        if (inL) W = shift_on ? sm.x[js][sidx - 1] + c : sm.x[js][sidx - 1];
+                        const double s = W + x1b + x2a + x0a;
+                        x1a = div_by_diag(s - b1a, dc0 + dr);
+                        sm.x[js][sidx] = x1a;
+                    }
+                } else {  // red cell is c1
+                    if (in1) {
+                        double E = 0.0;
+                        if (inR) E = shift_on ? sm.x[js][sidx + 2] + c : sm.x[js][sidx + 2];
+                        const double s = x1a + E + x2b + x0b;
+                        x1b = div_by_diag(s - b1b, dc1 + dr);
+                        sm.x[js][sidx + 1] = x1b;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // refill the slot freed two iterations ago
+        if (t == 0 && k + kAheadSweep <= klast) issue_row(sm, P, xin, b, k + kAheadSweep, a, ncopy);
+        // -- stage 2: black half-sweep of row j = k-2
+        {
+            const int j = k - 2;
+            if (active && j >= r0 - 1 && j >= 0 && j < P.ny) {
+                const int js = (j + 2 * kRing) % kRing;
+                const double dr = row_diag(P, j);
+                if ((j & 1) == 0) {  // black cell is c1
+                    if (in1) {
+                        const double E = inR ? sm.x[js][sidx + 2] : 0.0;
+                        const double s = x2a + E + x3b + x1b;
+                        x2b = div_by_diag(s - b2b, dc1 + dr);
+                        sm.x[js][sidx + 1] = x2b;
+                    }
+                } else {  // black cell is c0
+                    if (in0) {
+                        const double W = inL ? sm.x[js][sidx - 1] : 0.0;
+                        const double s = W + x2b + x3a + x1a;
+                        x2a = div_by_diag(s - b2a, dc0 + dr);
+                        sm.x[js][sidx] = x2a;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // -- stage 3: residual of row j = k-3, tile sums, store
+        {
+            const int j = k - 3;
+            if (j >= r0 && j < r1) {
+                if (owned) {
+                    const int js = (j + 2 * kRing) % kRing;
+                    const double dr = row_diag(P, j);
+                    double ra = 0.0, rb = 0.0;
+                    if (in0) {
+                        const double W = inL ? sm.x[js][sidx - 1] : 0.0;
+                        const double ax = W + x3b + x4a + x2a - (dc0 + dr) * x3a;
+                        ra = b3a - ax;
+                        mx = max_drop_nan(mx, fabs(ra));
+                        nan |= (ra != ra);
+                        sx = sx + x3a;
+                    }
+                    if (in1) {
+                        const double E = inR ? sm.x[js][sidx + 2] : 0.0;
+                        const double ax = x3a + E + x4b + x2b - (dc1 + dr) * x3b;
+                        rb = b3b - ax;
+                        mx = max_drop_nan(mx, fabs(rb));
+                        nan |= (rb != rb);
+                        sx = sx + x3b;
+                    }
+                    double* dst = xout + int64_t(j) * P.pitch + c0;
+                    if (in0 && in1) *reinterpret_cast<double2*>(dst) = make_double2(x3a, x3b);
+                    else if (in0) dst[0] = x3a;
+                    tacc = tacc + (ra + rb);
+                }
+                if (j % P.tile == P.tile - 1 || j == P.ny - 1) {  // tile row-block complete
+                    if (t < kPairs) {
+                        const double tsum = group_sum(tacc, g);
+                        if ((t % g) == 0 && in0) P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                    }
+                    tacc = 0.0;
+                }
+            }
+        }
+        // rotate the register window
+        x4a = x3a, x4b = x3b, x3a = x2a, x3b = x2b, x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b;
+        b3a = b2a, b3b = b2b, b2a = b1a, b2b = b1b, b1a = b0a, b1b = b0b;
+    }
+    pass_epilogue(sm, P, kFine, mx, sx, nan);
+}
+
+// ---- PROLONG / RESID body: x' = x + c + P ce, residual, restriction ---------
+__device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prolong) {
+    const int a = blockIdx.x * kW;
+    const int r0 = blockIdx.y * P.H, r1 = min(r0 + P.H, P.ny);
+    const double* xin = st.buf[st.cur];
+    double* xout = st.buf[st.cur ^ 1];
+    const double* b = st.b;
+    const bool shift_on = st.has_shift != 0;
+    const double c = st.shift;
+
+    const int t = threadIdx.x;
+    const bool owned = t < kPairs;
+    const bool halo = (t == kPairs) || (t == kPairs + 1);
+    const bool active = owned || halo;
+    const int c0 = owned ? a + 2 * t : (t == kPairs ? a - 2 : a + kW);
+    const int sidx = c0 - (a - 4);
+    const bool in0 = active && c0 >= 0 && c0 < P.nx, in1 = active && c0 + 1 >= 0 && c0 + 1 < P.nx;
+    const bool inL = active && c0 - 1 >= 0 && c0 - 1 < P.nx, inR = active && c0 + 2 < P.nx && c0 + 2 >= 0;
+    const double dc0 = col_diag(P, c0), dc1 = col_diag(P, c0 + 1);
+    const uint32_t ncopy = uint32_t(((min(a + kW + 4, P.nx + 5) - (a - 4)) + 1) & ~1);
+    // prolongation geometry of this thread's columns (TileAxis::locate_cell)
+    int I0a = 0, I1a = 0, I0b = 0, I1b = 0;
+    double sa = 0, dxa = 1, sb = 0, dxb = 1;
+    if (prolong) {
+        if (in0) I0a = P.ax.k0[c0], I1a = P.ax.k1[c0], sa = P.ax.t[c0], dxa = P.ax.dk[c0];
+        if (in1) I0b = P.ax.k0[c0 + 1], I1b = P.ax.k1[c0 + 1], sb = P.ax.t[c0 + 1], dxb = P.ax.dk[c0 + 1];
+    }
+
+    if (t == 0) {
+        for (int s = 0; s < kRing; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int kfirst = r0 - 1, klast = r1;
+    if (t == 0)
+        for (int k = kfirst; k <= min(klast, kfirst + kAheadRes - 1); ++k) issue_row(sm, P, xin, b, k, a, ncopy);
+
+    double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, b0a = 0, b0b = 0, b1a = 0, b1b = 0;
+    double mx = 0.0, sx = 0.0, tacc = 0.0;
+    int nan = 0;
+    const int g = P.tile >> 1;
+    for (int k = kfirst; k <= klast; ++k) {
+        const int slot = (k + 2 * kRing) % kRing;
+        const uint32_t parity = uint32_t(((k - kfirst) / kRing) & 1);
+        mbar_wait(&sm.bar[slot], parity);
+        const bool rk = k >= 0 && k < P.ny;
+        if (active) {
+            const double2 xv = *reinterpret_cast<const double2*>(&sm.x[slot][sidx]);
+            const double2 bv = *reinterpret_cast<const double2*>(&sm.b[slot][sidx]);
+            double va = (rk && in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
+            double vb = (rk && in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
+            if (prolong && rk) {  // coarsening.hpp:495-500
+                const double tt = P.ay.t[k], dy = P.ay.dk[k];
+                const int J0 = P.ay.k0[k], J1 = P.ay.k1[k];
+                if (in0)
+                    va += ((dxa - sa) * ((dy - tt) * P.ce.at(I0a, J0) + tt * P.ce.at(I0a, J1)) +
+                           sa * ((dy - tt) * P.ce.at(I1a, J0) + tt * P.ce.at(I1a, J1))) /
+                          (dxa * dy);
+                if (in1)
+                    vb += ((dxb - sb) * ((dy - tt) * P.ce.at(I0b, J0) + tt * P.ce.at(I0b, J1)) +
+                           sb * ((dy - tt) * P.ce.at(I1b, J0) + tt * P.ce.at(I1b, J1))) /
+                          (dxb * dy);
+            }
+            x0a = va, x0b = vb;
+            b0a = bv.x, b0b = bv.y;
+            *reinterpret_cast<double2*>(&sm.x[slot][sidx]) = make_double2(va, vb);
+        }
+        __syncthreads();
+        if (t == 0 && k + kAheadRes <= klast) issue_row(sm, P, xin, b, k + kAheadRes, a, ncopy);
+        const int j = k - 1;
+        if (j >= r0 && j < r1) {
+            if (owned) {
+                const int js = (j + 2 * kRing) % kRing;
+                const double dr = row_diag(P, j);
+                double ra = 0.0, rb = 0.0;
+                if (in0) {
+                    const double W = inL ? sm.x[js][sidx - 1] : 0.0;
+                    const double ax = W + x1b + x2a + x0a - (dc0 + dr) * x1a;
+                    ra = b1a - ax;
+                    mx = max_drop_nan(mx, fabs(ra));
+                    nan |= (ra != ra);
+                    sx = sx + x1a;
+                }
+                if (in1) {
+                    const double E = inR ? sm.x[js][sidx + 2] : 0.0;
+                    const double ax = x1a + E + x2b + x0b - (dc1 + dr) * x1b;
+                    rb = b1b - ax;
+                    mx = max_drop_nan(mx, fabs(rb));
+                    nan |= (rb != rb);
+                    sx = sx + x1b;
+                }
+                if (prolong) {
+                    double* dst = xout + int64_t(j) * P.pitch + c0;
+                    if (in0 && in1) *reinterpret_cast<double2*>(dst) = make_double2(x1a, x1b);
+                    else if (in0) dst[0] = x1a;
+                }
+                tacc = tacc + (ra + rb);
+            }
+            if (j % P.tile == P.tile - 1 || j == P.ny - 1) {
+                if (t < kPairs) {
+                    const double tsum = group_sum(tacc, g);
+                    if ((t % g) == 0 && in0) P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                }
+                tacc = 0.0;
+            }
+        }
+        x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b, b1a = b0a, b1b = b0b;
+    }
+    pass_epilogue(sm, P, prolong ? kProlong : kResid, mx, sx, nan);
+}
+
+__global__ void __launch_bounds__(kThreads) fine_pass_kernel(Params P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
+    if (st.phase == kFine) sweep_body(sm, P, st);
+    else if (st.phase == kProlong) prolong_body(sm, P, st, true);
+    else if (st.phase == kResid) prolong_body(sm, P, st, false);
+}
+// final anchor + copy into the caller's field: x = buf[cur] + c
+__global__ void finalize_kernel(Params P, View xuser) {
+    const Ctl* s = P.ctl;
+    const double* src = s->buf[s->cur];
+    const bool sh = s->has_shift != 0;
+    const double c = s->shift;
+    if (s->cur == 0 && !sh) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= P.nx) return;
+    const double v = src[int64_t(j) * P.pitch + i];
+    xuser.at(i, j) = sh ? v + c : v;
+}
+
+
+void launch_fine_pass(const Params& P, dim3 grid, size_t smem, cudaStream_t st) {
+    fine_pass_kernel<<<grid, kThreads, smem, st>>>(P);
+}
+size_t fine_pass_smem() { return sizeof(Smem); }
+void set_fine_pass_smem(size_t bytes) {
+    ISMG_CUDA(cudaFuncSetAttribute(fine_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+void launch_finalize(const Params& P, View xuser, cudaStream_t st) {
+    finalize_kernel<<<dim3((P.nx + 255) / 256, P.ny), 256, 0, st>>>(P, xuser);
+}
+
+}  // namespace fz
+}  // namespace ismgb

@@ -1,0 +1,203 @@
+// fused_host.cu — host side of the fused hot path: engine setup, CUDA-graph
+// capture of [coarse-visit, fine-pass] slots, and the solve driver that polls
+// the device-resident phase once per graph launch.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "fused_impl.cuh"
+
+namespace ismgb {
+using namespace fz;
+
+struct FusedEngine {
+    Solver* s = nullptr;
+    Params P{};
+    Ctl* d_ctl = nullptr;
+    Ctl* h_ctl = nullptr;  // pinned
+    DevBuf scratch;        // second ping-pong buffer
+    int* d_log = nullptr;
+    std::vector<int> h_log;
+    cudaGraphExec_t graph = nullptr;
+    double* coarse_backup = nullptr;
+    size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
+    int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs
+    TmGeom tm{};
+    double* tm_spec = nullptr;
+    int graph_slots = 0;
+    size_t smem = 0;
+    dim3 grid;
+    cudaEvent_t ev = nullptr;
+};
+
+bool fused_supported(const Solver& s) {
+    if (s.cfg.scheme != ISMG_SCHEME_ISMG && s.cfg.scheme != ISMG_SCHEME_GMG) return false;
+    if (s.bc.px() || s.bc.py()) return false;
+    const int tile = s.g.tile;
+    if (tile < 2 || tile > 64 || (tile & (tile - 1)) != 0) return false;  // tile | 256, lanes fold in a warp
+    if (s.levels.empty()) return false;
+    const CoarseOpH& h = s.levels.front().h;
+    for (size_t k = 0; k < size_t(h.ncx) * h.ncy; ++k)
+        if (h.w[k] == 0.0) return false;  // singular coarse row: op-level path raises
+    return true;
+}
+
+static void capture_graph(FusedEngine& e, int slots) {
+    Ctx& c = *e.s->ctx;
+    if (e.graph) cudaGraphExecDestroy(e.graph);
+    e.graph = nullptr;
+    cudaGraph_t g;
+    ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < slots; ++k) {
+        if (e.coarse_kind == 2)
+            launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
+        else if (e.coarse_kind == 1)
+            launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
+        else
+            launch_coarse_global(e.P, c.stream);
+        launch_fine_pass(e.P, e.grid, e.smem, c.stream);
+    }
+    ISMG_CUDA(cudaStreamEndCapture(c.stream, &g));
+    ISMG_CUDA(cudaGraphInstantiate(&e.graph, g, 0));
+    cudaGraphDestroy(g);
+    e.graph_slots = slots;
+}
+
+FusedEngine* make_fused(Solver& s) {
+    auto* e = new FusedEngine();
+    e->s = &s;
+    Ctx& c = *s.ctx;
+    LevelDev& L = s.levels.front();
+    e->scratch.alloc(s.g.nx + 1, s.g.ny + 1);
+    Params& P = e->P;
+    P.nx = s.g.nx, P.ny = s.g.ny, P.pitch = e->scratch.pitch;
+    P.tile = s.g.tile, P.ncx = L.h.ncx, P.ncy = L.h.ncy;
+    P.H = std::max(P.tile, 128 / P.tile * P.tile);
+    P.nstrips = (P.nx + kW - 1) / kW;
+    P.nchunks = (P.ny + P.H - 1) / P.H;
+    P.bc = s.bc;
+    P.singular = s.singular ? 1 : 0;
+    P.nslots = L.h.stencil_points();
+    P.tol_fine = s.cfg.tol_fine, P.tol_coarse = s.cfg.tol_coarse, P.stall = s.cfg.stall_factor;
+    P.max_total = s.cfg.max_total_sweeps;
+    P.ncells = double(int64_t(P.nx) * P.ny);
+    P.cb = L.b->view();
+    P.ce = L.x->view();
+    P.w = L.d_w;
+    P.ax = L.ax, P.ay = L.ay;
+    const int nb = P.nstrips * P.nchunks;
+    ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 2 * nb));
+    ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned)));
+    ISMG_CUDA(cudaMemset(P.ticket, 0, sizeof(unsigned)));
+    P.visit_cap = int(std::min<long long>(P.max_total + 2, 1 << 22));
+    ISMG_CUDA(cudaMalloc(&e->d_log, sizeof(int) * 2 * P.visit_cap));
+    P.visit_log = e->d_log;
+    ISMG_CUDA(cudaMalloc(&e->d_ctl, sizeof(Ctl)));
+    ISMG_CUDA(cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
+    P.ctl = e->d_ctl;
+    e->grid = dim3(P.nstrips, P.nchunks);
+    e->smem = fine_pass_smem();
+    set_fine_pass_smem(e->smem);
+    ISMG_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
+    // coarse-visit kernel: TMEM-resident rhs when the operator allows it,
+    // else shared-memory iterate, else the global-memory wavefront
+    std::vector<double> spec;
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "tmem" | "smem" | "global"
+    const bool allow_tmem = !force || std::string(force) == "tmem";
+    const bool allow_smem = !force || std::string(force) != "global";
+    if (allow_tmem && tmem_coarse_plan(L.h, e->tm, spec, e->coarse_smem)) {
+        e->coarse_kind = 2;
+        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
+        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.PP));
+        set_coarse_tmem_smem(e->coarse_smem);
+    } else if (allow_smem && size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double) <= 200 * 1024) {
+        e->coarse_kind = 1;
+        e->coarse_smem = size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double);
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, e->coarse_smem));
+        set_coarse_smem(e->coarse_smem);
+    }
+    (void)c;
+    return e;
+}
+
+void destroy_fused(FusedEngine* e) {
+    if (!e) return;
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    e->scratch.free();
+    cudaFree(e->P.part);
+    cudaFree(e->P.ticket);
+    cudaFree(e->d_log);
+    cudaFree(e->coarse_backup);
+    cudaFree(e->tm_spec);
+    cudaFree(e->d_ctl);
+    cudaFreeHost(e->h_ctl);
+    if (e->ev) cudaEventDestroy(e->ev);
+    delete e;
+}
+
+void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics& M, bool, double**) {
+    FusedEngine& e = *s.fused;
+    Ctx& c = *s.ctx;
+    if (x.buf.pitch != e.P.pitch || b.buf.pitch != e.P.pitch)
+        fail(ISMG_ERR_INTERNAL, "fused path: field pitch mismatch");
+    k_zero_ghosts(c, x.view());  // cycles.hpp:106
+    Ctl init{};
+    init.phase = kResid;
+    init.converged = 1;
+    init.cur = 0;
+    init.buf[0] = x.buf.origin();
+    init.buf[1] = e.scratch.origin();
+    init.b = b.buf.origin();
+    *e.h_ctl = init;
+    ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    // launch batches of [coarse-visit, fine-pass] slots until the phase is done
+    int slots = 8;
+    long long launched_slots = 0;
+    int since_poll = 0;
+    for (;;) {
+        if (!e.graph || e.graph_slots != slots) capture_graph(e, slots);
+        ISMG_CUDA(cudaGraphLaunch(e.graph, c.stream));
+        launched_slots += slots;
+        ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+        ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
+        ISMG_CUDA(cudaEventSynchronize(e.ev));
+        s.last.host_syncs += 1;
+        ++since_poll;
+        if (e.h_ctl->phase == kDone) break;
+        if (launched_slots > 4 * (s.cfg.max_total_sweeps + 8)) fail(ISMG_ERR_INTERNAL, "fused solve did not terminate");
+        slots = std::min(64, slots * 2);
+    }
+    (void)since_poll;
+    launch_finalize(e.P, x.view(), c.stream);
+    ISMG_CUDA(cudaGetLastError());
+    const Ctl& st = *e.h_ctl;
+    // replay the sweep sequence into the metrics (lap_equiv order, metrics.hpp:46-56)
+    const int nv = std::min(st.nvisits, e.P.visit_cap);
+    e.h_log.resize(size_t(2) * std::max(nv, 1));
+    if (nv > 0)
+        ISMG_CUDA(cudaMemcpyAsync(e.h_log.data(), e.d_log, sizeof(int) * 2 * nv, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    s.visit_log.assign(e.h_log.begin(), e.h_log.begin() + 2 * nv);
+    const int64_t cells = int64_t(s.g.nx) * s.g.ny;
+    const LevelDev& L = s.levels.front();
+    const int64_t ccells = int64_t(L.h.ncx) * L.h.ncy;
+    for (int v = 0; v < nv; ++v) {
+        M.restriction();
+        for (int k = 0; k < e.h_log[2 * v]; ++k) M.sweep(false, L.h.stencil_points(), ccells);
+        for (int k = 0; k < e.h_log[2 * v + 1]; ++k) M.sweep(true, 5, cells);
+    }
+    for (long long k = 0; k < st.prolongations; ++k) M.prolongation();
+    rep.converged = st.converged;
+    rep.nan_seen = st.nan_seen;
+    rep.fine_sweeps = st.fine;
+    rep.coarse_sweeps = st.coarse;
+    rep.residual = st.r;
+    s.last.fine_passes = st.fine;
+    s.last.prolong_passes = st.prolongations;
+    s.last.coarse_visits = st.coarse_launches;
+    s.last.kernel_launches = 2 * launched_slots + 2;
+}
+
+}  // namespace ismgb

@@ -1,0 +1,141 @@
+// fused_impl.cuh — shared definitions of the fused hot path (fine_pass.cu,
+// coarse.cu, fused_host.cu): phases, the device-resident solve state, kernel
+// parameters and the mbarrier / TMA bulk-copy helpers.
+#pragma once
+
+#include "kernels.cuh"
+#include "solver.h"
+
+namespace ismgb {
+namespace fz {
+
+constexpr int kW = 256;                 // owned columns per CTA strip
+constexpr int kPairs = kW / 2;          // owned column pairs (one per thread)
+constexpr int kThreads = kPairs + 32;   // + one warp for the two halo pairs
+constexpr int kRing = 8;                // smem row ring
+constexpr int kRowCap = kW + 8;         // smem row: columns [a-4, a+W+4)
+constexpr int kAheadSweep = kRing - 4;  // rows prefetched ahead (sweep)
+constexpr int kAheadRes = kRing - 2;    // rows prefetched ahead (prolong/residual)
+constexpr int kCoarseThreads = 1024;
+constexpr int kCoarseSmemThreads = 512;
+
+enum Phase : int { kFine = 0, kCoarse = 1, kProlong = 2, kResid = 3, kDone = 4 };
+
+// Device-resident solve state (one per solver).
+struct Ctl {
+    int phase;
+    int converged;
+    int cur;        // fine iterate lives in buf[cur]; buf[0] is the caller's x
+    int has_shift;  // singular: a pending anchor shift applies to buf[cur]
+    int nan_seen;
+    int nvisits;
+    long long total, fine, coarse, restrictions, prolongations;
+    long long passes, coarse_launches;
+    double r, prev, shift, rc;
+    double* buf[2];
+    const double* b;
+};
+
+struct Params {
+    int nx, ny;
+    int64_t pitch;  // shared by every fine field of this grid
+    int tile, ncx, ncy, H, nstrips, nchunks;
+    PBC bc;
+    int singular, nslots;
+    double tol_fine, tol_coarse, stall;
+    long long max_total;
+    double ncells;
+    Ctl* ctl;
+    View cb, ce;  // coarse rhs / correction
+    const double* w;
+    AxisDev ax, ay;
+    double* part;  // 2 per CTA: max|r|, sum x
+    unsigned* ticket;
+    int* visit_log;  // (coarse sweeps, fine sweeps) per coarse visit
+    int visit_cap;
+    double* coarse_scratch;  // reduction scratch for the coarse kernel
+};
+
+// ---- PTX helpers: mbarrier + TMA bulk copy ----------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct Smem {
+    double x[kRing][kRowCap];
+    double b[kRing][kRowCap];
+    uint64_t bar[kRing];
+    double red[2][32];
+    int last;
+};
+
+// Issue the TMA bulk copies of fine row `row` (x and b) into ring slot.
+__device__ __forceinline__ void issue_row(Smem& sm, const Params& P, const double* xin, const double* b, int row,
+                                          int a, uint32_t ncopy) {
+    const int slot = (row + 2 * kRing) % kRing;  // row may be -3
+    fence_proxy_async();
+    mbar_expect_tx(&sm.bar[slot], 2u * ncopy * 8u);
+    const int64_t off = int64_t(row) * P.pitch + (a - 4);
+    bulk_load(sm.x[slot], xin + off, ncopy * 8u, &sm.bar[slot]);
+    bulk_load(sm.b[slot], b + off, ncopy * 8u, &sm.bar[slot]);
+}
+
+__device__ __forceinline__ double row_diag(const Params& P, int j) {
+    return ((j > 0) ? 1.0 : face_weight(P.bc.k[ISMG_SIDE_SOUTH])) +
+           ((j < P.ny - 1) ? 1.0 : face_weight(P.bc.k[ISMG_SIDE_NORTH]));
+}
+__device__ __forceinline__ double col_diag(const Params& P, int i) {
+    return ((i > 0) ? 1.0 : face_weight(P.bc.k[ISMG_SIDE_WEST])) +
+           ((i < P.nx - 1) ? 1.0 : face_weight(P.bc.k[ISMG_SIDE_EAST]));
+}
+
+// Tile-sum fold over the g = tile/2 lanes of one coarse cell (g divides 32).
+__device__ __forceinline__ double group_sum(double v, int g) {
+    for (int o = g >> 1; o > 0; o >>= 1) v = v + __shfl_down_sync(kFull, v, o);
+    return v;
+}
+
+// launchers (each in the translation unit of its kernel)
+void launch_fine_pass(const Params& P, dim3 grid, size_t smem, cudaStream_t st);
+size_t fine_pass_smem();
+void set_fine_pass_smem(size_t bytes);
+void launch_finalize(const Params& P, View xuser, cudaStream_t st);
+void launch_coarse_global(const Params& P, cudaStream_t st);
+void launch_coarse_smem(const Params& P, double* backup, size_t smem, cudaStream_t st);
+void set_coarse_smem(size_t bytes);
+
+// TMEM-resident coarse visit (coarse.cu): geometry of the diagonal layout.
+struct TmGeom {
+    int ncx, ncy, PP, ring;
+    bool five;
+    double stdw[9];
+};
+bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem);
+void launch_coarse_tmem(const Params& P, const TmGeom& T, const double* spec, double* backup, size_t smem,
+                        cudaStream_t st);
+void set_coarse_tmem_smem(size_t bytes);
+
+}  // namespace fz
+}  // namespace ismgb

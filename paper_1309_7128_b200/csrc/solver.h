@@ -53,6 +53,7 @@ struct Solver {
     std::unique_ptr<Field> res;    // residual scratch of the op-level paths
     FusedEngine* fused = nullptr;
     ismg_solve_stats last{};
+    std::vector<int> visit_log;  // (coarse sweeps, fine sweeps) per outer iteration of the last solve
     int mode = 0;  // 0 = auto (fused hot path when supported), 1 = op-level reference order
 
     Solver(Ctx* c, const ismg_grid_spec& g, const ismg_cycle_config& cfg);

@@ -167,6 +167,14 @@ class PressureSolver:
         _lib.call("ismg_solver_last_stats", self.h, C.byref(s))
         return {k: getattr(s, k) for k, _ in CSolveStats._fields_}
 
+    def visit_log(self):
+        """[(coarse sweeps, fine sweeps)] per outer iteration of the last fused solve."""
+        n = C.c_size_t()
+        _lib.call("ismg_solver_visit_log", self.h, None, 0, C.byref(n))
+        buf = (C.c_int32 * (2 * max(n.value, 1)))()
+        _lib.call("ismg_solver_visit_log", self.h, buf, n.value, C.byref(n))
+        return [(buf[2 * k], buf[2 * k + 1]) for k in range(n.value)]
+
     # -- op-level reference calls (device fields) ---------------------------
     def rbgs_sweep(self, x: DeviceField, b: DeviceField) -> None:
         _lib.call("ismg_rbgs_sweep", self.h, x.h, b.h)

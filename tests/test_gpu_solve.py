@@ -134,3 +134,32 @@ def test_zero_rhs_and_budget(dev):
         cfg = CycleConfig(scheme=s, tile=8, depth=3, tol_fine=1e-12, tol_coarse=1e-12, max_total_sweeps=3)
         rep = P.PressureSolver(cavity(32, 32), cfg).solve(ScalarField(32, 32), b, RunMetrics(1024))
         assert not rep.converged and rep.fine_sweeps + rep.coarse_sweeps <= 3
+
+
+@pytest.mark.parametrize("kernel", ["tmem", "smem", "global"])
+@pytest.mark.parametrize("which", ["lid96", "jet48x96"])
+def test_coarse_visit_kernels_match_oracle(dev, port, monkeypatch, kernel, which):
+    """Every coarse-visit kernel of the fused path (TMEM-resident rhs,
+    shared-memory iterate, global wavefront) reproduces the reference's
+    per-step counts; the jet (non-singular: no anchoring) must be bit-exact
+    in the coarse solve, so its fields match to round-off of the tree sums."""
+    P = dev
+    monkeypatch.setenv("ISMG_COARSE_KERNEL", kernel)
+    if which == "lid96":
+        case = setup_lid_cavity(96, 100.0)
+        case.dt = 100.0 / 96
+        cfg, nsteps = CycleConfig(tile=8), 15
+    else:
+        case = setup_jet(48, 96, 0.1, 8)
+        cfg, nsteps = CycleConfig(tile=8), 8
+    case.steps, case.t_max, case.steady_tol = nsteps, 0.0, 0.0
+    res = P.run_case(case, cfg)
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, _ = port.run_steps(case.grid, cfg, st, nsteps)
+    got = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in res.metrics.rows]
+    want = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in rows]
+    assert got == want
+    for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
+                 (res.state.p.data, st.p.data)):
+        assert rel_l2(a, b) <= REL_L2

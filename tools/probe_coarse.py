@@ -1,0 +1,16 @@
+"""Coarse-visit profiling probe: one lid-cavity step with a capped sweep budget."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1309_7128_b200 as P
+from paper_1309_7128_b200.api import CycleConfig, FluidState, RunMetrics, setup_lid_cavity
+
+n, tile, budget = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+case = setup_lid_cavity(n, 1000.0)
+case.dt = 1000.0 / n
+solver = P.PressureSolver(case.grid, CycleConfig(tile=tile, max_total_sweeps=budget))
+st = FluidState(case.grid); st.dt, st.nu = case.dt, case.nu
+ds = P.DeviceState(case.grid, solver.ctx, st)
+m = RunMetrics(n * n)
+ds.step(solver, m)
+s = solver.last_stats()
+print("solve %.1f ms, I_f %d I_c %d, visits %s" % (s["solve_ms"], m.rows[-1].fine_sweeps, m.rows[-1].coarse_sweeps, solver.visit_log()[:4]))
