@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: ISM pressure solve (arXiv 1309.7128) on B200 — fine-grid cell-updates/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+Workload (BASELINE.json configs[1]): lid-driven
+cavity 4096^2, Re = 1000, u_lid = 0.1, h = 1, dt = Re/n, ISM two-level with
+32h tiles (coarse 128^2), tol_fine 1e-6, tol_coarse 1e-5, 20000-sweep budget,
+stall 0.9, fp64, synthetic quiescent start (seed 0).
+
+A "step" is one projection step (predictor, divergence, ISM pressure solve,
+correction). W warm-up steps run on a throwaway state; the K timed steps are
+steps 1..K of the time integration from the quiescent start (the reference arm
+samples step 1 as well). Metric = fine-grid cell-updates per second =
+sum(I_f) * nx * ny / time.
+
+  value   device-resident state, CUDA events around the K steps on the library
+          stream (torch's current stream), max over ranks.
+  e2e     the same K steps through the public API with the state in pinned host
+          memory: per step H2D of (u, v, p), step, D2H of (u, v, p).
+  roofline  the dominant kernel (fused fine pass, 24 algorithmic B/cell) timed
+          with CUDA events per launch on the library stream, against the
+          measured HBM copy bandwidth in MEASURED_PEAKS.json.
+  cpu_baseline  the unmodified reference (oracle/_ref, compiled from its own
+          headers) on 1 host core, bounded sample: step 1 capped at 3000 sweeps.
+
+--impl reference runs that reference CPU path with every host core it can use:
+the reference solve is single-threaded (cycles.hpp; bench.hpp:266-313 only
+parallelises independent cases), so it runs one independent capped step-1
+sample per core and reports the aggregate cell-updates/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+N_DEFAULT = 4096
+RE = 1000.0
+TILE = 32
+REF_SAMPLE_CAP = 3000  # max_total_sweeps of the bounded CPU sample (step 1)
+
+
+def workload(n=N_DEFAULT):
+    from paper_1309_7128_b200.api import CycleConfig, setup_lid_cavity
+    case = setup_lid_cavity(n, RE)
+    case.dt = RE / n  # dt = Re/n: the reference default dt = 1 diverges
+    case.steps, case.t_max, case.steady_tol = 10 ** 9, 0.0, 0.0
+    cfg = CycleConfig(tile=TILE, tol_fine=1e-6, tol_coarse=1e-5, max_total_sweeps=20000, stall_factor=0.9)
+    return case, cfg
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except Exception:
+                continue
+            for k, name in enumerate(names):
+                if len(p) > 3 + k and p[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(kind, n=N_DEFAULT, cap=REF_SAMPLE_CAP):
+    """One bounded reference sample: step 1 with the sweep budget capped. Returns (I_f, seconds)."""
+    from pyoracle import Oracle
+    from paper_1309_7128_b200.api import FluidState
+    case, cfg = workload(n)
+    cfg.max_total_sweeps = cap
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    o = Oracle(kind)
+    t0 = time.perf_counter()
+    rows, secs = o.run_steps(case.grid, cfg, st, 1)
+    wall = time.perf_counter() - t0
+    return rows[0].fine_sweeps, (secs if secs is not None else wall)
+
+
+def cpu_kind():
+    from pyoracle import available
+    return "reference" if available("reference") else "port"
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the unmodified reference CPU solve on all host cores."""
+    if rank != 0:
+        return
+    import psutil
+    kind = cpu_kind()
+    n = N_DEFAULT
+    ncpu = os.cpu_count() or 1
+    mem_gb = psutil.virtual_memory().available / 2 ** 30
+    cores = max(1, min(ncpu, int(mem_gb // 2.5)))
+    cells = n * n
+
+    def round_(cap):
+        res = [None] * cores
+
+        def work(k):
+            res[k] = cpu_sample(kind, n, cap)
+        th = [threading.Thread(target=work, args=(k,)) for k in range(cores)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        round_(200)
+    tot_if, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        i_f, t = round_(REF_SAMPLE_CAP)
+        tot_if += i_f
+        tot_t += t
+    value = tot_if * cells / tot_t
+    sample = ("step 1 of lid %d^2 Re 1000 (dt = Re/n, tile 32) capped at %d sweeps, %d independent single-threaded "
+              "solves in parallel (the reference solve has no intra-solve threading)" % (n, REF_SAMPLE_CAP, cores))
+    line = {
+        "impl": "reference", "metric": "fine-grid cell-updates/s", "value": value, "unit": "cell-updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "lid-driven cavity %dx%d Re=1000, ISM 32h two-level (config 2)" % (n, n),
+                   "global_batch": 1, "seq_len": 0, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1309_7128_b200 as P
+    from paper_1309_7128_b200.api import FluidState, RunMetrics
+
+    torch.cuda.set_device(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(local_rank, stream.cuda_stream)
+    n = N_DEFAULT
+    case, cfg = workload(n)
+    g = case.grid
+    cells = n * n
+    solver = P.PressureSolver(g, cfg, ctx)
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+    def fresh_state():
+        st = FluidState(g)
+        st.dt, st.nu = case.dt, case.nu
+        return st
+
+    # --- warm-up on a throwaway state
+    ds = P.DeviceState(g, ctx, fresh_state())
+    mw = RunMetrics(cells)
+    for _ in range(args.warmup):
+        ds.step(solver, mw)
+    del ds
+    torch.cuda.synchronize()
+
+    # --- timed region: device-resident state, steps 1..K
+    ds = P.DeviceState(g, ctx, fresh_state())
+    m = RunMetrics(cells)
+    l0 = ctx.launch_count()
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            ds.step(solver, m)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - l0
+    fine = sum(r.fine_sweeps for r in m.rows)
+    coarse = sum(r.coarse_sweeps for r in m.rows)
+    if dist:
+        t = torch.tensor([ms, float(fine)], dtype=torch.float64, device="cuda")
+        tt = t.clone()
+        tdist.all_reduce(tt[0:1], op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(tt[1:2], op=tdist.ReduceOp.SUM)
+        ms_max, fine_all = float(tt[0]), float(tt[1])
+    else:
+        ms_max, fine_all = ms, float(fine)
+    value = fine_all * cells / (ms_max * 1e-3)
+
+    # --- e2e: public API with the state in pinned host memory
+    def pinned(nelem):
+        return torch.empty(nelem, dtype=torch.float64, pin_memory=True).numpy()
+
+    host = fresh_state()
+    for name in ("u_data", "v_data"):
+        a = pinned(getattr(host.vel, name).size)
+        a[:] = 0.0
+        setattr(host.vel, name, a)
+    pdata = pinned(host.p.data.size)
+    pdata[:] = 0.0
+    host.p.data = pdata
+    ds2 = P.DeviceState(g, ctx)
+    m2 = RunMetrics(cells)
+    bytes_io = (host.vel.u_data.nbytes + host.vel.v_data.nbytes + host.p.data.nbytes)
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        ds2.upload(host)  # H2D: u, v, p (+ t, dt, nu, step)
+        ds2.step(solver, m2)
+        ds2.download(host)  # D2H: u, v, p
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    fine2 = sum(r.fine_sweeps for r in m2.rows)
+    if dist:
+        t = torch.tensor([e2e_ms, float(fine2)], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t[0:1], op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(t[1:2], op=tdist.ReduceOp.SUM)
+        e2e_ms, fine2 = float(t[0]), float(t[1])
+    e2e_value = fine2 * cells / (e2e_ms * 1e-3)
+
+    # --- roofline: the fused fine pass, CUDA events per launch on the library stream
+    hbm, src = peaks()
+    xs = P.DeviceField(n, n, ctx)
+    bs = P.DeviceField(n, n, ctx)
+    # rhs of the timed run's first step, rebuilt through the public kernels
+    vel = P.DeviceVelocity(n, n, ctx)
+    vstar = P.DeviceVelocity(n, n, ctx)
+    pf = P.DeviceField(n, n, ctx)
+    P.apply_velocity_bc(vel, g)
+    vstar.upload(vel.download())
+    P.predictor(vel, pf, case.dt, case.nu, g, vstar)
+    P.apply_velocity_bc(vstar, g)
+    P.divergence(vstar, g, bs, g.h * g.h / case.dt)
+    pass_ms = solver.bench_fine_pass(xs, bs, 20)
+    alg_bytes = 24.0 * cells
+    achieved = alg_bytes / (pass_ms * 1e-3) / 1e9
+
+    # --- CPU baseline: the reference on one core, bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        kind = cpu_kind()
+        i_f, secs = cpu_sample(kind, n)
+        cpu = {"value": i_f * cells / secs, "unit": "cell-updates/s", "cores": 1, "kind": kind,
+               "sample": "step 1 of the same workload capped at %d sweeps (I_f %d in %.1f s)" % (REF_SAMPLE_CAP, i_f,
+                                                                                               secs)}
+
+    if rank == 0:
+        line = {
+            "metric": "fine-grid cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if dist else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (quiescent lid-driven cavity, seed 0)",
+            "config": {"workload": "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (config 2)" % (n, n),
+                       "global_batch": 1, "seq_len": 0,
+                       "parallelism": ("replicas x%d" % world) if dist else "single GPU",
+                       "steps_timed": "projection steps 1..%d" % args.steps,
+                       "l2": "inputs larger than L2 (x, scratch, b: 3 x 134 MB vs 126 MB L2)",
+                       "fine_sweeps": int(fine_all), "coarse_sweeps": int(coarse)},
+            "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": bytes_io,
+                    "d2h_bytes_per_step": bytes_io},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "kernel": "fine_pass_kernel (sweep mode)",
+                         "alg_bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms, "peak_source": src},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and "RANK" in os.environ:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1 and "RANK" in os.environ:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -247,6 +247,15 @@ int ismg_solver_last_stats(const ismg_solver* s, ismg_solve_stats* out);
  * (c0, f0, c1, f1, ...). *n receives the number of visits; at most cap visits
  * are written (out may be NULL to query). */
 int ismg_solver_visit_log(const ismg_solver* s, int32_t* out, size_t cap, size_t* n);
+/* Measurement hook: run `iters` fused fine passes (red + black half-sweeps,
+ * residual, tile-sum restriction, anchor sum; 24 algorithmic bytes per cell)
+ * back to back on (x, b) with CUDA events around each on the context stream;
+ * *ms_per_pass = mean event time. Requires the fused path (ISMG/GMG,
+ * non-periodic, power-of-two tile <= 64). x is relaxed in place. */
+int ismg_bench_fine_pass(ismg_solver* s, ismg_field* x, const ismg_field* b, int iters,
+                         double* ms_per_pass);
+/* kernels launched through this context so far (stream order) */
+int ismg_ctx_launch_count(const ismg_ctx* ctx, int64_t* out);
 
 /* ---- projection step ------------------------------------------------------ */
 /* apply_scalar_bc — field.hpp:77-96 */

@@ -82,6 +82,8 @@ SIGNATURES = {
     "ismg_solve_host": [VP, DP, DP, C.c_size_t, R, M, C.c_int64],
     "ismg_solver_last_stats": [VP, C.POINTER(CSolveStats)],
     "ismg_solver_visit_log": [VP, I32P, C.c_size_t, C.POINTER(C.c_size_t)],
+    "ismg_bench_fine_pass": [VP, VP, VP, C.c_int, DP],
+    "ismg_ctx_launch_count": [VP, C.POINTER(C.c_int64)],
     "ismg_apply_scalar_bc": [VP, G, VP],
     "ismg_apply_velocity_bc": [VP, G, VP],
     "ismg_divergence": [VP, G, VP, VP, C.c_double],

@@ -399,6 +399,27 @@ int ismg_solver_visit_log(const ismg_solver* s, int32_t* out, size_t cap, size_t
     });
 }
 
+int ismg_bench_fine_pass(ismg_solver* s, ismg_field* x, const ismg_field* b, int iters, double* ms_per_pass) {
+    return guard([&] {
+        Solver& v = S(s);
+        need(ms_per_pass, "ms_per_pass");
+        fine_dims(v, F(x));
+        fine_dims(v, F(b));
+        if (!v.fused) fail(ISMG_ERR_INVALID_ARGUMENT, "bench_fine_pass: solver has no fused path");
+        if (iters < 1) fail(ISMG_ERR_INVALID_ARGUMENT, "bench_fine_pass: iters must be >= 1");
+        ISMG_CUDA(cudaSetDevice(v.ctx->device));
+        *ms_per_pass = fused_bench_fine_pass(v, F(x), F(b), iters);
+    });
+}
+
+int ismg_ctx_launch_count(const ismg_ctx* c, int64_t* out) {
+    return guard([&] {
+        need(c, "ctx");
+        need(out, "out");
+        *out = c->impl.launches;
+    });
+}
+
 int ismg_solver_last_stats(const ismg_solver* s, ismg_solve_stats* out) {
     return guard([&] {
         need(s, "solver");

@@ -29,6 +29,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int sms = 148;
+    long long launches = 0;  // kernels launched through this context (stream order)
     Scratch s;
     Comm* comm = nullptr;
     Ctx(int device, cudaStream_t stream);

@@ -24,9 +24,8 @@ namespace ismgb {
 namespace fz {
 
 // ---- per-CTA epilogue + control flow (last CTA) ------------------------------
-__device__ void fine_decide(const Params& P, int mode, double r, double sum, int nan) {
+__device__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
     Ctl* s = P.ctl;
-    if (nan) s->nan_seen = 1;
     s->passes += 1;
     s->r = r;
     if (P.singular) {  // anchor after every residual check (field.hpp:49,53-59)
@@ -34,6 +33,7 @@ __device__ void fine_decide(const Params& P, int mode, double r, double sum, int
         s->has_shift = 1;
     }
     if (mode != kResid) s->cur ^= 1;
+    if (s->hold) return;  // ismg_bench_fine_pass: repeat the same pass kind
     auto to_coarse = [&]() {
         s->restrictions += 1;
         if (s->nvisits < P.visit_cap) {
@@ -41,7 +41,13 @@ __device__ void fine_decide(const Params& P, int mode, double r, double sum, int
             P.visit_log[2 * s->nvisits + 1] = 0;
         }
         s->nvisits += 1;
-        s->phase = kCoarse;
+        s->rc = rc0;
+        if (rc0 > P.tol_coarse) {
+            s->phase = kCoarse;
+        } else {  // zero-sweep visit: no prolongation, relax again (cycles.hpp:125,138,146)
+            s->prev = r;
+            s->phase = kFine;
+        }
     };
     if (mode == kFine) {  // cycles.hpp:147-161
         s->total += 1;
@@ -77,15 +83,20 @@ __device__ void fine_decide(const Params& P, int mode, double r, double sum, int
     }
 }
 
-__device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, int nan) {
+// cm = max |tile sum| this CTA wrote to cb: the coarse entry residual
+// coarse_residual(ce = 0, cb) = max|cb| (cycles.hpp:122-123) is complete when
+// the pass ends, so a visit that needs no coarse sweep is decided here.
+__device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, double cm, int nan) {
     const int nb = gridDim.x * gridDim.y;
     const int bid = blockIdx.y * gridDim.x + blockIdx.x;
     double bm = block_max(mx, sm.red[0]);
     double bs = block_sum(sx, sm.red[1]);
+    double bc = block_max(cm, sm.red[2]);
     int anynan = __syncthreads_or(nan);
     if (threadIdx.x == 0) {
-        P.part[2 * bid] = bm;
-        P.part[2 * bid + 1] = bs;
+        P.part[3 * bid] = bm;
+        P.part[3 * bid + 1] = bs;
+        P.part[3 * bid + 2] = bc;
         if (anynan) P.ctl->nan_seen = 1;
         __threadfence();
         const unsigned t = atomicAdd(P.ticket, 1u);
@@ -94,15 +105,17 @@ __device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, do
     __syncthreads();
     if (!sm.last) return;
     __threadfence();
-    double m = 0.0, s = 0.0;
+    double m = 0.0, s = 0.0, c = 0.0;
     for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-        m = fmax(m, __ldcg(&P.part[2 * k]));
-        s += __ldcg(&P.part[2 * k + 1]);
+        m = fmax(m, __ldcg(&P.part[3 * k]));
+        s += __ldcg(&P.part[3 * k + 1]);
+        c = fmax(c, __ldcg(&P.part[3 * k + 2]));
     }
     m = block_max(m, sm.red[0]);
     s = block_sum(s, sm.red[1]);
+    c = block_max(c, sm.red[2]);
     if (threadIdx.x == 0) {
-        fine_decide(P, mode, m, s, 0);
+        fine_decide(P, mode, m, s, c);
         *P.ticket = 0u;
         __threadfence();
     }
@@ -141,7 +154,7 @@ __device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
     // vertical register window: x{d} = row k-d of this thread's column pair
     double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, x3a = 0, x3b = 0, x4a = 0, x4b = 0;
     double b0a = 0, b0b = 0, b1a = 0, b1b = 0, b2a = 0, b2b = 0, b3a = 0, b3b = 0;
-    double mx = 0.0, sx = 0.0, tacc = 0.0;
+    double mx = 0.0, sx = 0.0, tacc = 0.0, cm = 0.0;
     int nan = 0;
     const int g = P.tile >> 1;
 
@@ -243,7 +256,10 @@ __device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
                 if (j % P.tile == P.tile - 1 || j == P.ny - 1) {  // tile row-block complete
                     if (t < kPairs) {
                         const double tsum = group_sum(tacc, g);
-                        if ((t % g) == 0 && in0) P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                        if ((t % g) == 0 && in0) {
+                        P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                        cm = max_drop_nan(cm, fabs(tsum));
+                    }
                     }
                     tacc = 0.0;
                 }
@@ -253,7 +269,7 @@ __device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
         x4a = x3a, x4b = x3b, x3a = x2a, x3b = x2b, x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b;
         b3a = b2a, b3b = b2b, b2a = b1a, b2b = b1b, b1a = b0a, b1b = b0b;
     }
-    pass_epilogue(sm, P, kFine, mx, sx, nan);
+    pass_epilogue(sm, P, kFine, mx, sx, cm, nan);
 }
 
 // ---- PROLONG / RESID body: x' = x + c + P ce, residual, restriction ---------
@@ -294,7 +310,7 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
         for (int k = kfirst; k <= min(klast, kfirst + kAheadRes - 1); ++k) issue_row(sm, P, xin, b, k, a, ncopy);
 
     double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, b0a = 0, b0b = 0, b1a = 0, b1b = 0;
-    double mx = 0.0, sx = 0.0, tacc = 0.0;
+    double mx = 0.0, sx = 0.0, tacc = 0.0, cm = 0.0;
     int nan = 0;
     const int g = P.tile >> 1;
     for (int k = kfirst; k <= klast; ++k) {
@@ -357,14 +373,17 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
             if (j % P.tile == P.tile - 1 || j == P.ny - 1) {
                 if (t < kPairs) {
                     const double tsum = group_sum(tacc, g);
-                    if ((t % g) == 0 && in0) P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                    if ((t % g) == 0 && in0) {
+                        P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                        cm = max_drop_nan(cm, fabs(tsum));
+                    }
                 }
                 tacc = 0.0;
             }
         }
         x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b, b1a = b0a, b1b = b0b;
     }
-    pass_epilogue(sm, P, prolong ? kProlong : kResid, mx, sx, nan);
+    pass_epilogue(sm, P, prolong ? kProlong : kResid, mx, sx, cm, nan);
 }
 
 __global__ void __launch_bounds__(kThreads) fine_pass_kernel(Params P) {

@@ -87,7 +87,7 @@ FusedEngine* make_fused(Solver& s) {
     P.w = L.d_w;
     P.ax = L.ax, P.ay = L.ay;
     const int nb = P.nstrips * P.nchunks;
-    ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 2 * nb));
+    ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 3 * nb));
     ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned)));
     ISMG_CUDA(cudaMemset(P.ticket, 0, sizeof(unsigned)));
     P.visit_cap = int(std::min<long long>(P.max_total + 2, 1 << 22));
@@ -110,7 +110,7 @@ FusedEngine* make_fused(Solver& s) {
         e->coarse_kind = 2;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
         ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
-        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.PP));
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.pitch));
         set_coarse_tmem_smem(e->coarse_smem);
     } else if (allow_smem && size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double) <= 200 * 1024) {
         e->coarse_kind = 1;
@@ -137,6 +137,48 @@ void destroy_fused(FusedEngine* e) {
     delete e;
 }
 
+// Benchmark hook: `iters` fused sweep passes (red, black, residual, tile sums,
+// anchor sum) back to back on (x, b), each bracketed by CUDA events on the
+// context stream. Returns the mean event time per pass in ms. x is relaxed in
+// place (ping-pong through the scratch buffer).
+double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters) {
+    FusedEngine& e = *s.fused;
+    Ctx& c = *s.ctx;
+    if (x.buf.pitch != e.P.pitch || b.buf.pitch != e.P.pitch)
+        fail(ISMG_ERR_INTERNAL, "fused path: field pitch mismatch");
+    k_zero_ghosts(c, x.view());
+    Ctl init{};
+    init.phase = kFine;
+    init.hold = 1;
+    init.buf[0] = x.buf.origin();
+    init.buf[1] = e.scratch.origin();
+    init.b = b.buf.origin();
+    *e.h_ctl = init;
+    ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    std::vector<cudaEvent_t> ev(size_t(iters) + 1);
+    for (auto& v : ev) ISMG_CUDA(cudaEventCreate(&v));
+    ISMG_CUDA(cudaEventRecord(ev[0], c.stream));
+    for (int k = 0; k < iters; ++k) {
+        launch_fine_pass(e.P, e.grid, e.smem, c.stream);
+        ISMG_CUDA(cudaEventRecord(ev[size_t(k) + 1], c.stream));
+    }
+    c.launches += iters;
+    ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    double total = 0.0;
+    for (int k = 0; k < iters; ++k) {
+        float ms = 0.f;
+        ISMG_CUDA(cudaEventElapsedTime(&ms, ev[size_t(k)], ev[size_t(k) + 1]));
+        total += ms;
+    }
+    for (auto& v : ev) cudaEventDestroy(v);
+    if (e.h_ctl->cur != 0) {  // leave the relaxed iterate in the caller's field
+        ISMG_CUDA(cudaMemcpyAsync(x.buf.base, e.scratch.base, x.buf.bytes, cudaMemcpyDeviceToDevice, c.stream));
+        c.sync();
+    }
+    return total / iters;
+}
+
 void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics& M, bool, double**) {
     FusedEngine& e = *s.fused;
     Ctx& c = *s.ctx;
@@ -159,6 +201,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     for (;;) {
         if (!e.graph || e.graph_slots != slots) capture_graph(e, slots);
         ISMG_CUDA(cudaGraphLaunch(e.graph, c.stream));
+        c.launches += 2 * slots;
         launched_slots += slots;
         ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
         ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
@@ -171,6 +214,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     }
     (void)since_poll;
     launch_finalize(e.P, x.view(), c.stream);
+    c.launches += 1;
     ISMG_CUDA(cudaGetLastError());
     const Ctl& st = *e.h_ctl;
     // replay the sweep sequence into the metrics (lap_equiv order, metrics.hpp:46-56)

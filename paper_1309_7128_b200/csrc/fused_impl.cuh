@@ -29,6 +29,7 @@ struct Ctl {
     int has_shift;  // singular: a pending anchor shift applies to buf[cur]
     int nan_seen;
     int nvisits;
+    int hold;  // benchmark hook: passes leave the phase unchanged
     long long total, fine, coarse, restrictions, prolongations;
     long long passes, coarse_launches;
     double r, prev, shift, rc;
@@ -49,7 +50,7 @@ struct Params {
     View cb, ce;  // coarse rhs / correction
     const double* w;
     AxisDev ax, ay;
-    double* part;  // 2 per CTA: max|r|, sum x
+    double* part;  // 3 per CTA: max|r|, sum x, max|tile sum|
     unsigned* ticket;
     int* visit_log;  // (coarse sweeps, fine sweeps) per coarse visit
     int visit_cap;
@@ -87,7 +88,7 @@ struct Smem {
     double x[kRing][kRowCap];
     double b[kRing][kRowCap];
     uint64_t bar[kRing];
-    double red[2][32];
+    double red[3][32];
     int last;
 };
 
@@ -128,7 +129,11 @@ void set_coarse_smem(size_t bytes);
 
 // TMEM-resident coarse visit (coarse.cu): geometry of the diagonal layout.
 struct TmGeom {
-    int ncx, ncy, PP, ring;
+    int ncx, ncy;
+    int PP;     // diagonal slots per row (period of the skew)
+    int pitch;  // smem row pitch = PP + 6 (3 mirrored slots each side), = 1 mod 16
+    int ring;
+    int kind;   // interior stencil: 0 generic (stdw), 1 ISMG (-3, 1/2, 1/4), 2 five-point (-4, 1)
     bool five;
     double stdw[9];
 };

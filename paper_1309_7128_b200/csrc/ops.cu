@@ -384,7 +384,11 @@ __global__ void add_interior_kernel(View d, View s) {  // field.hpp:60-66
 
 // ---------------------------------------------------------------------------
 // launchers
-#define LAUNCH_CHECK() ISMG_CUDA(cudaGetLastError())
+#define LAUNCH_CHECK()                  \
+    do {                                \
+        ISMG_CUDA(cudaGetLastError());  \
+        c.launches += 1;                \
+    } while (0)
 
 void k_fill(Ctx& c, View f, double v) {
     dim3 grid((f.nx + 2 + 255) / 256, f.ny + 2);

@@ -94,5 +94,6 @@ FusedEngine* make_fused(Solver& s);
 void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics& M, bool leave_pending_shift,
                  double** pending_shift);
 void destroy_fused(FusedEngine* e);
+double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters);
 
 }  // namespace ismgb

@@ -42,6 +42,11 @@ class Context:
     def synchronize(self) -> None:
         _lib.call("ismg_ctx_synchronize", self.h)
 
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _lib.call("ismg_ctx_launch_count", self.h, C.byref(n))
+        return n.value
+
     def __del__(self):
         try:
             if getattr(self, "h", None) and _lib._lib is not None:
@@ -166,6 +171,12 @@ class PressureSolver:
         s = CSolveStats()
         _lib.call("ismg_solver_last_stats", self.h, C.byref(s))
         return {k: getattr(s, k) for k, _ in CSolveStats._fields_}
+
+    def bench_fine_pass(self, x: DeviceField, b: DeviceField, iters: int) -> float:
+        """Mean CUDA-event time (ms) of one fused fine pass on (x, b)."""
+        ms = C.c_double()
+        _lib.call("ismg_bench_fine_pass", self.h, x.h, b.h, int(iters), C.byref(ms))
+        return ms.value
 
     def visit_log(self):
         """[(coarse sweeps, fine sweeps)] per outer iteration of the last fused solve."""
