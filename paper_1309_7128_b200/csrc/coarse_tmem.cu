@@ -19,7 +19,10 @@
 //    interior rows are the ISMG (-3; 1/2; 1/4) or five-point (-4; 1) stencil bit
 //    for bit; boundary-ring cells take a divergent path with their nine
 //    coefficients from shared memory.
+#include <array>
 #include <cmath>
+#include <cstdint>
+#include <cstring>
 
 #include "fused_impl.cuh"
 
@@ -29,8 +32,10 @@ namespace fz {
 namespace {
 
 constexpr int kLagT = 8;         // wavefront steps between consecutive sweeps
-constexpr int kMaxGroupT = 128;  // sweeps per checkpointed group
+constexpr int kMaxGroupT = 512;  // sweeps per checkpointed group
 constexpr int kTmH = 8;          // warps per TMEM lane quadrant
+constexpr int kTmU = 2;          // cells per warp-iteration
+constexpr int kPredCap = 32;     // cap of the predicted first group of a visit
 constexpr int kTmThreads = 128 * kTmH;
 
 struct TmSmem {
@@ -104,6 +109,17 @@ __device__ __forceinline__ double apply_w(const double* w, const Nbr& v, double 
     return kResidual ? bIJ - acc : (bIJ - acc) / w[0];
 }
 
+// a / -3 correctly rounded, without the DDIV sequence (~115-cycle latency):
+// Markstein's correction with y = RN(1/b): q = RN(a y), r = a - b q (exact by
+// FMA), RN(q + r y) = RN(a / b). Checked against __ddiv_rn bit for bit on
+// 1.2e9 random operands per divisor (tools/verify_div3.cu).
+__device__ __forceinline__ double div_m3(double a) {
+    constexpr double y = -1.0 / 3.0;
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, -3.0, a);
+    return __fma_rn(r, y, q);
+}
+
 // Compile-time interior stencils (host-verified against the built operator).
 template <bool kResidual, int Kind>
 __device__ __forceinline__ double apply_std(const TmGeom& T, const Nbr& v, double bIJ) {
@@ -117,14 +133,14 @@ __device__ __forceinline__ double apply_std(const TmGeom& T, const Nbr& v, doubl
         acc += 0.25 * v.nw;
         acc += 0.25 * v.se;
         acc += 0.25 * v.sw;
-        return kResidual ? bIJ - acc : (bIJ - acc) / -3.0;
+        return kResidual ? bIJ - acc : div_m3(bIJ - acc);
     } else if constexpr (Kind == 2) {  // five-point interior row: C -4, E/W/N/S 1
         double acc = kResidual ? -4.0 * v.c : 0.0;
         acc += 1.0 * v.e;
         acc += 1.0 * v.w;
         acc += 1.0 * v.n;
         acc += 1.0 * v.s;
-        return kResidual ? bIJ - acc : (bIJ - acc) / -4.0;
+        return kResidual ? bIJ - acc : (bIJ - acc) * -0.25;  // exact: power-of-two divisor
     } else {
         return apply_w<kResidual>(T.stdw, v, bIJ, T.five);
     }
@@ -136,16 +152,129 @@ __device__ __forceinline__ double tm_cell(const TmGeom& T, const double* rc, con
     const Nbr v = gather(rc, T.pitch, s, kResidual, T.five);
     const bool special = (I == 0) | (I == T.ncx - 1) | (J == 0) | (J == T.ncy - 1);
     if (!special) return apply_std<kResidual, Kind>(T, v, bIJ);
+    // boundary ring: stencil class table, 9 weights + RN(1/w0) per class
+    const int* ring_cls = reinterpret_cast<const int*>(spec + 10 * T.ncls);
+    const double* wc = spec + 10 * ring_cls[ring_index(T, I, J)];
     double w[9];
-    const int ri = ring_index(T, I, J);
 #pragma unroll
-    for (int sl = 0; sl < 9; ++sl) w[sl] = spec[sl * T.ring + ri];
-    return apply_w<kResidual>(w, v, bIJ, T.five);
+    for (int sl = 0; sl < 9; ++sl) w[sl] = wc[sl];
+    if (kResidual) return apply_w<true>(w, v, bIJ, T.five);
+    double acc = 0.0;  // update: coarsening.hpp:558-565
+    if (w[1] != 0.0) acc += w[1] * v.e;
+    if (w[2] != 0.0) acc += w[2] * v.w;
+    if (w[3] != 0.0) acc += w[3] * v.n;
+    if (w[4] != 0.0) acc += w[4] * v.s;
+    if (!T.five) {
+        if (w[5] != 0.0) acc += w[5] * v.ne;
+        if (w[6] != 0.0) acc += w[6] * v.nw;
+        if (w[7] != 0.0) acc += w[7] * v.se;
+        if (w[8] != 0.0) acc += w[8] * v.sw;
+    }
+    const double num = bIJ - acc;
+    if (!T.fastdiv) return num / w[0];
+    const double y = wc[9];  // Markstein: exact RN(num / w0)
+    const double q = __dmul_rn(num, y);
+    const double r = __fma_rn(-q, w[0], num);
+    return __fma_rn(r, y, q);
+}
+
+// max over the warp of non-negative doubles through two 32-bit REDUX steps
+// (ordering of non-negative doubles = ordering of their (hi, lo) words)
+__device__ __forceinline__ double warp_max_nonneg(double m) {
+    const unsigned hi = unsigned(__double2hiint(m)), lo = unsigned(__double2loint(m));
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    return __hiloint2double(int(mh), int(ml));
+}
+
+// U independent cells per warp-iteration: the cells one warp handles at one
+// step lie on diagonals 8 kTmH apart, so none reads another's slot; their
+// TMEM loads, gathers, arithmetic and stores are issued as batches and the
+// fp64 dependency chains overlap.
+template <int Kind, int U>
+__device__ void tm_group(const TmGeom& T, double* xs, const double* spec, uint32_t tq, TmSmem& cs, int G,
+                         bool residuals) {
+    const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, h = warp >> 2;
+    const int J = 32 * q + lane;
+    const bool rowok = J < T.ncy;
+    double* rc = row_ptr(xs, T, J);
+    const int PP = T.PP;
+    const int jmin = 32 * q, jmax = min(32 * q + 31, T.ncy - 1);
+    const int dlo = 2 * jmin, dhi = min(dmax, 2 * jmax + T.ncx - 1);
+    if (residuals)
+        for (int k = threadIdx.x; k < 4 * kMaxGroupT; k += blockDim.x) (&cs.wmax[0][0])[k] = 0.0;
+    __syncthreads();
+    const int tau_end = dmax + kLagT * (G - 1) + (residuals ? 4 : 0);
+    constexpr int kStride = kLagT * kTmH;  // diagonal distance of consecutive cells of one warp
+    for (int tau = 0; tau <= tau_end; ++tau) {
+        if (jmin < T.ncy) {
+            for (int phase = 0; phase < (residuals ? 2 : 1); ++phase) {
+                const int base = phase == 0 ? tau : tau - 4;
+                if (base < dlo) continue;
+                const int g_lo = max(0, (base - dhi + kLagT - 1) / kLagT), g_hi = min(G - 1, (base - dlo) / kLagT);
+                const int g0 = g_lo + (((h - g_lo) % kTmH) + kTmH) % kTmH;
+                if (g0 > g_hi) continue;
+                const int d0 = base - kLagT * g0;
+                int s0 = (d0 + 4) % PP;
+                for (int gb = g0; gb <= g_hi; gb += U * kTmH) {
+                    uint32_t lo[U], hi[U];
+                    int I[U], s[U];
+                    bool ok[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int g = gb + u * kTmH;
+                        const int d = base - kLagT * g;
+                        s[u] = s0;
+                        s0 -= kStride;
+                        s0 += s0 < 0 ? PP : 0;  // kStride < PP (plan)
+                        I[u] = d - 2 * J;
+                        ok[u] = (g <= g_hi) && rowok && I[u] >= 0 && I[u] < T.ncx;
+                        if (g <= g_hi) tm_ld2(tq + 2u * uint32_t(d & 255), lo[u], hi[u]);  // warp-uniform
+                    }
+                    tm_wait_ld();
+                    double out[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const double bIJ = __hiloint2double(int(hi[u]), int(lo[u]));
+                        out[u] = 0.0;
+                        if (ok[u]) {
+                            out[u] = phase == 0 ? tm_cell<false, Kind>(T, rc, spec, I[u], J, s[u], bIJ)
+                                                : tm_cell<true, Kind>(T, rc, spec, I[u], J, s[u], bIJ);
+                        }
+                    }
+                    if (phase == 0) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (ok[u]) {
+                                const int su = s[u];
+                                rc[su] = out[u];
+                                if (su < 3) rc[su + PP] = out[u];  // mirrored end slots
+                                if (su >= PP - 3) rc[su - PP] = out[u];
+                            }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int g = gb + u * kTmH;
+                            if (g > g_hi) break;
+                            double m = fabs(out[u]);
+                            m = (m != m) ? 0.0 : m;  // std::max drops NaN
+                            m = warp_max_nonneg(m);
+                            // (q, g) belongs to this warp alone: accumulate over steps
+                            if (lane == 0) cs.wmax[q][g] = fmax(cs.wmax[q][g], m);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
 }
 
 template <int Kind>
-__device__ void tm_group(const TmGeom& T, double* xs, const double* spec, uint32_t tq, TmSmem& cs, int G,
-                         bool residuals) {
+__device__ void tm_group_v1(const TmGeom& T, double* xs, const double* spec, uint32_t tq, TmSmem& cs, int G,
+                            bool residuals) {
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3, h = warp >> 2;
@@ -225,7 +354,9 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
         const int JJ = k / ncx, II = k - JJ * ncx;
         xs[k] = P.cb.at(II, JJ);
     }
-    for (int k = threadIdx.x; k < 9 * T.ring; k += blockDim.x) spec[k] = spec_g[k];
+    // class table (10 doubles per class) followed by the ring's class ids
+    const int spec_words = 10 * T.ncls + (T.ring + 1) / 2;
+    for (int k = threadIdx.x; k < spec_words; k += blockDim.x) spec[k] = spec_g[k];
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
@@ -244,12 +375,14 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
     double rc = st->rc;  // max|cb|, formed by the fine pass that restricted
     const long long budget = P.max_total - st->total;
     long long done = 0;
-    int G = 1;
+    // first group = the previous visit's sweep count (visits of one solve
+    // have similar lengths), then doubling
+    int G = max(1, min(st->pred, kPredCap));
     while (rc > P.tol_coarse && done < budget) {
         if (budget - done < G) G = int(budget - done);
         if (G > 1)
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) backup[k] = xs[k];  // checkpoint
-        tm_group<Kind>(T, xs, spec, tq, cs, G, true);
+        tm_group<Kind, kTmU>(T, xs, spec, tq, cs, G, true);
         if (threadIdx.x == 0) {
             int first = -1;
             double rg = 0.0;
@@ -269,7 +402,7 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
         if (first >= 0 && first < G - 1) {  // overshoot: restore and replay first+1 sweeps
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) xs[k] = backup[k];
             __syncthreads();
-            tm_group<Kind>(T, xs, spec, tq, cs, first + 1, false);
+            tm_group<Kind, kTmU>(T, xs, spec, tq, cs, first + 1, false);
             done += first + 1;
             break;
         }
@@ -301,6 +434,7 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(cs.tmem_base));
     if (threadIdx.x == 0) {
         st->coarse_launches += 1;
+        if (done > 0) st->pred = int(done);
         st->total += done;
         st->coarse += done;
         st->rc = rc;
@@ -325,7 +459,10 @@ bool same_bits(double a, double b) { return a == b && std::signbit(a) == std::si
 bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem) {
     if (op.px || op.py || op.ncx > 256 || op.ncy > 128 || op.ncx < 3 || op.ncy < 3) return false;
     T.ncx = op.ncx, T.ncy = op.ncy, T.five = op.five_point;
-    T.PP = (op.ncx + 2) + ((11 - (op.ncx + 2) % 16) + 16) % 16;  // PP = 11 (mod 16) -> pitch = 1 (mod 16)
+    // PP >= ncx + 2 (distinct ghost slots), > 8 kTmH (one fold per step), and
+    // PP = 11 (mod 16) so the row pitch PP + 6 = 1 (mod 16) doubles
+    const int pp_min = std::max(op.ncx + 2, kLagT * kTmH + 1);
+    T.PP = pp_min + ((11 - pp_min % 16) + 16) % 16;
     T.pitch = T.PP + 6;
     T.ring = 2 * op.ncx + 2 * op.ncy;
     for (int sl = 0; sl < 9; ++sl) T.stdw[sl] = op.at(sl, 1, 1);
@@ -344,16 +481,48 @@ bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec,
     }
     if (is_ismg) T.kind = 1;
     if (is_five) T.kind = 2;
-    spec.assign(size_t(9) * T.ring, 0.0);
-    auto put = [&](int r, int I, int J) {
-        for (int sl = 0; sl < 9; ++sl) spec[size_t(sl) * T.ring + r] = op.at(sl, I, J);
+    // boundary ring -> classes of identical stencils (walls are translation invariant)
+    std::vector<std::array<double, 9>> cls;
+    std::vector<int> ring_cls(size_t(T.ring), 0);
+    auto classify = [&](int r, int I, int J) {
+        std::array<double, 9> w;
+        for (int sl = 0; sl < 9; ++sl) w[sl] = op.at(sl, I, J);
+        size_t c = 0;
+        for (; c < cls.size(); ++c) {
+            bool eq = true;
+            for (int sl = 0; sl < 9 && eq; ++sl) eq = same_bits(cls[c][sl], w[sl]);
+            if (eq) break;
+        }
+        if (c == cls.size()) cls.push_back(w);
+        ring_cls[size_t(r)] = int(c);
     };
-    for (int I = 0; I < op.ncx; ++I) put(I, I, 0), put(op.ncx + I, I, op.ncy - 1);
-    for (int J = 0; J < op.ncy; ++J) put(2 * op.ncx + J, 0, J), put(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
-    for (size_t r = 0; r < size_t(T.ring); ++r)
-        if (spec[r] == 0.0) return false;  // singular ring row: the op-level path raises
+    for (int I = 0; I < op.ncx; ++I) classify(I, I, 0), classify(op.ncx + I, I, op.ncy - 1);
+    for (int J = 0; J < op.ncy; ++J) classify(2 * op.ncx + J, 0, J), classify(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
+    T.ncls = int(cls.size());
+    if (T.ncls > 1024) return false;
+    // Markstein's correction RN(q + r y) == RN(a / w0) for y = RN(1/w0): spot-check
+    // every class divisor on random operands before trusting it
+    T.fastdiv = 1;
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    for (const auto& w : cls) {
+        if (w[0] == 0.0) return false;  // singular ring row: the op-level path raises
+        const double b = w[0], y = 1.0 / b;
+        for (int k = 0; k < 20000 && T.fastdiv; ++k) {
+            st ^= st << 13, st ^= st >> 7, st ^= st << 17;
+            const double a = std::ldexp(double(st >> 11) * 0x1.0p-53 + 0.5, int((st >> 3) % 120) - 60) *
+                             ((st & 1) ? -1.0 : 1.0);
+            const double q = a * y, r = std::fma(-q, b, a), mk = std::fma(r, y, q);
+            if (!same_bits(mk, a / b)) T.fastdiv = 0;
+        }
+    }
+    spec.assign(size_t(10) * T.ncls + size_t(T.ring + 1) / 2, 0.0);
+    for (int c = 0; c < T.ncls; ++c) {
+        for (int sl = 0; sl < 9; ++sl) spec[size_t(10) * c + sl] = cls[size_t(c)][size_t(sl)];
+        spec[size_t(10) * c + 9] = 1.0 / cls[size_t(c)][0];
+    }
+    std::memcpy(spec.data() + size_t(10) * T.ncls, ring_cls.data(), sizeof(int) * ring_cls.size());
     const size_t xs_doubles = std::max(size_t(op.ncy + 2) * T.pitch, size_t(op.ncx) * op.ncy);
-    smem = (xs_doubles + size_t(9) * T.ring) * sizeof(double);
+    smem = (xs_doubles + spec.size()) * sizeof(double);
     return smem <= 200 * 1024;
 }
 

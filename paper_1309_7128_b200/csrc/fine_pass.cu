@@ -1,4 +1,4 @@
-// fused.cu — the hot path: device-resident solve_two_level (cycles.hpp:101-165).
+// fine_pass.cu — the hot path: device-resident solve_two_level (cycles.hpp:101-165).
 //
 // One fine iteration = ONE HBM pass (24 B/cell: read x, b; write x):
 //   x' = x + c (pending anchor, smoother.hpp:145-148)  -> red half-sweep ->
@@ -24,7 +24,7 @@ namespace ismgb {
 namespace fz {
 
 // ---- per-CTA epilogue + control flow (last CTA) ------------------------------
-__device__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
+__device__ __forceinline__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
     Ctl* s = P.ctl;
     s->passes += 1;
     s->r = r;
@@ -86,7 +86,7 @@ __device__ void fine_decide(const Params& P, int mode, double r, double sum, dou
 // cm = max |tile sum| this CTA wrote to cb: the coarse entry residual
 // coarse_residual(ce = 0, cb) = max|cb| (cycles.hpp:122-123) is complete when
 // the pass ends, so a visit that needs no coarse sweep is decided here.
-__device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, double cm, int nan) {
+__device__ __forceinline__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, double cm, int nan) {
     const int nb = gridDim.x * gridDim.y;
     const int bid = blockIdx.y * gridDim.x + blockIdx.x;
     double bm = block_max(mx, sm.red[0]);
@@ -122,7 +122,37 @@ __device__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, do
 }
 
 // ---- SWEEP body: anchor-shift, red, black, residual, restriction ------------
-__device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
+// ---- per-thread column geometry -------------------------------------------
+// Threads 0..kPairs-1 own the column pairs (a + 2t, a + 2t + 1) of the strip;
+// thread kPairs holds the left halo pair (a-2, a-1), kPairs+1 the right halo
+// pair (a+W, a+W+1). The last lane of the halo warp issues the TMA copies.
+struct ColGeom {
+    int t, c0, sidx;
+    bool owned, active, in0, in1, inL, inR;
+    double dc0, dc1;  // column part of the diagonal (W + E faces)
+    __device__ __forceinline__ ColGeom(const Params& P, int a) {
+        t = threadIdx.x;
+        owned = t < kPairs;
+        const bool halo = (t == kPairs) || (t == kPairs + 1);
+        active = owned || halo;
+        c0 = owned ? a + 2 * t : (t == kPairs ? a - 2 : a + kW);
+        sidx = c0 - (a - 4);
+        in0 = active && c0 >= 0 && c0 < P.nx;
+        in1 = active && c0 + 1 >= 0 && c0 + 1 < P.nx;
+        inL = active && c0 - 1 >= 0 && c0 - 1 < P.nx;
+        inR = active && c0 + 2 >= 0 && c0 + 2 < P.nx;
+        dc0 = col_diag(P, c0);
+        dc1 = col_diag(P, c0 + 1);
+    }
+};
+
+constexpr int kProducer = kThreads - 1;  // TMA issuer (idle lane of the halo warp)
+
+// ---- SWEEP body: anchor-shift, red, black, residual, restriction ------------
+// Iteration k: load row k, red half-sweep of row k-1, black half-sweep of row
+// k-2, residual + store of row k-3 (each stage reads only rows the previous
+// stages have finished; see the file comment).
+__device__ __forceinline__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
     const int a = blockIdx.x * kW;
     const int r0 = blockIdx.y * P.H, r1 = min(r0 + P.H, P.ny);
     const double* xin = st.buf[st.cur];
@@ -130,136 +160,129 @@ __device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
     const double* b = st.b;
     const bool shift_on = st.has_shift != 0;
     const double c = st.shift;
-
-    const int t = threadIdx.x;
-    const bool owned = t < kPairs;
-    const bool halo = (t == kPairs) || (t == kPairs + 1);
-    const bool active = owned || halo;
-    const int c0 = owned ? a + 2 * t : (t == kPairs ? a - 2 : a + kW);
-    const int sidx = c0 - (a - 4);
-    const bool in0 = active && c0 >= 0 && c0 < P.nx, in1 = active && c0 + 1 >= 0 && c0 + 1 < P.nx;
-    const bool inL = active && c0 - 1 >= 0 && c0 - 1 < P.nx, inR = active && c0 + 2 < P.nx && c0 + 2 >= 0;
-    const double dc0 = col_diag(P, c0), dc1 = col_diag(P, c0 + 1);
+    const ColGeom cg(P, a);
+    const int t = cg.t, sidx = cg.sidx, c0 = cg.c0;
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    const double fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     const uint32_t ncopy = uint32_t(((min(a + kW + 4, P.nx + 5) - (a - 4)) + 1) & ~1);
+    const int tmask = P.tile - 1;  // power-of-two tile (fused_supported)
 
-    if (t == 0) {
+    if (t == kProducer) {
         for (int s = 0; s < kRing; ++s) mbar_init(&sm.bar[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     const int kfirst = r0 - 3, klast = r1 + 2;
-    if (t == 0)
+    if (t == kProducer)
         for (int k = kfirst; k <= min(klast, kfirst + kAheadSweep - 1); ++k) issue_row(sm, P, xin, b, k, a, ncopy);
 
-    // vertical register window: x{d} = row k-d of this thread's column pair
+    // vertical register window: x{d}, b{d}, dr{d} = row k-d of this column pair
     double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, x3a = 0, x3b = 0, x4a = 0, x4b = 0;
     double b0a = 0, b0b = 0, b1a = 0, b1b = 0, b2a = 0, b2b = 0, b3a = 0, b3b = 0;
+    double dr0 = 0, dr1 = 0, dr2 = 0, dr3 = 0;
     double mx = 0.0, sx = 0.0, tacc = 0.0, cm = 0.0;
     int nan = 0;
     const int g = P.tile >> 1;
 
     for (int k = kfirst; k <= klast; ++k) {
-        const int slot = (k + 2 * kRing) % kRing;
-        const uint32_t parity = uint32_t(((k - kfirst) / kRing) & 1);
+        const int slot = k & (kRing - 1);
+        const uint32_t parity = (uint32_t(k - kfirst) >> 3) & 1u;  // fill count of this slot, mod 2
         // -- load row k (raw + pending anchor shift), masked outside the domain
-        mbar_wait(&sm.bar[slot], parity);
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), parity);
         const bool rk = k >= 0 && k < P.ny;
-        if (active) {
+        dr0 = ((k > 0) ? 1.0 : fwS) + ((k < P.ny - 1) ? 1.0 : fwN);  // row part of smoother.hpp:60-61
+        if (cg.active) {
             const double2 xv = *reinterpret_cast<const double2*>(&sm.x[slot][sidx]);
             const double2 bv = *reinterpret_cast<const double2*>(&sm.b[slot][sidx]);
-            x0a = (rk && in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
-            x0b = (rk && in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
+            x0a = (rk && cg.in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
+            x0b = (rk && cg.in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
             b0a = bv.x;
             b0b = bv.y;
         }
-        // -- stage 1: red half-sweep of row j = k-1
+        // -- stage 1: red half-sweep of row j = k-1 (smoother.hpp:111-113)
         {
             const int j = k - 1;
-            if (active && j >= r0 - 2 && j >= 0 && j < P.ny) {
-                const int js = (j + 2 * kRing) % kRing;
-                const double dr = row_diag(P, j);
+            if (cg.active && j >= r0 - 2 && j >= 0 && j < P.ny) {
+                double* row = sm.x[j & (kRing - 1)];
                 if ((j & 1) == 0) {  // red cell is c0
-                    if (in0) {
+                    if (cg.in0) {
                         double W = 0.0;
-                        if (inL) W = shift_on ? sm.x[js][sidx - 1] + c : sm.x[js][sidx - 1];
+                        if (cg.inL) W = shift_on ? row[sidx - 1] + c : row[sidx - 1];
                         const double s = W + x1b + x2a + x0a;
-                        x1a = div_by_diag(s - b1a, dc0 + dr);
-                        sm.x[js][sidx] = x1a;
+                        x1a = div_by_diag(s - b1a, cg.dc0 + dr1);
+                        row[sidx] = x1a;
                     }
                 } else {  // red cell is c1
-                    if (in1) {
+                    if (cg.in1) {
                         double E = 0.0;
-                        if (inR) E = shift_on ? sm.x[js][sidx + 2] + c : sm.x[js][sidx + 2];
+                        if (cg.inR) E = shift_on ? row[sidx + 2] + c : row[sidx + 2];
                         const double s = x1a + E + x2b + x0b;
-                        x1b = div_by_diag(s - b1b, dc1 + dr);
-                        sm.x[js][sidx + 1] = x1b;
+                        x1b = div_by_diag(s - b1b, cg.dc1 + dr1);
+                        row[sidx + 1] = x1b;
                     }
                 }
             }
         }
-        __syncthreads();
-        // refill the slot freed two iterations ago
-        if (t == 0 && k + kAheadSweep <= klast) issue_row(sm, P, xin, b, k + kAheadSweep, a, ncopy);
+        // (no barrier: stage 2 reads red cells of row k-2 written one iteration
+        // ago; its N/S neighbours are this thread's own registers)
         // -- stage 2: black half-sweep of row j = k-2
         {
             const int j = k - 2;
-            if (active && j >= r0 - 1 && j >= 0 && j < P.ny) {
-                const int js = (j + 2 * kRing) % kRing;
-                const double dr = row_diag(P, j);
+            if (cg.active && j >= r0 - 1 && j >= 0 && j < P.ny) {
+                double* row = sm.x[j & (kRing - 1)];
                 if ((j & 1) == 0) {  // black cell is c1
-                    if (in1) {
-                        const double E = inR ? sm.x[js][sidx + 2] : 0.0;
+                    if (cg.in1) {
+                        const double E = cg.inR ? row[sidx + 2] : 0.0;
                         const double s = x2a + E + x3b + x1b;
-                        x2b = div_by_diag(s - b2b, dc1 + dr);
-                        sm.x[js][sidx + 1] = x2b;
+                        x2b = div_by_diag(s - b2b, cg.dc1 + dr2);
+                        row[sidx + 1] = x2b;
                     }
                 } else {  // black cell is c0
-                    if (in0) {
-                        const double W = inL ? sm.x[js][sidx - 1] : 0.0;
+                    if (cg.in0) {
+                        const double W = cg.inL ? row[sidx - 1] : 0.0;
                         const double s = W + x2b + x3a + x1a;
-                        x2a = div_by_diag(s - b2a, dc0 + dr);
-                        sm.x[js][sidx] = x2a;
+                        x2a = div_by_diag(s - b2a, cg.dc0 + dr2);
+                        row[sidx] = x2a;
                     }
                 }
             }
         }
-        __syncthreads();
-        // -- stage 3: residual of row j = k-3, tile sums, store
+        // -- stage 3: residual of row j = k-3 (smoother.hpp:134-137), tile sums, store
+        // (its horizontal neighbours were final one iteration ago)
         {
             const int j = k - 3;
             if (j >= r0 && j < r1) {
-                if (owned) {
-                    const int js = (j + 2 * kRing) % kRing;
-                    const double dr = row_diag(P, j);
+                if (cg.owned) {
+                    const double* row = sm.x[j & (kRing - 1)];
                     double ra = 0.0, rb = 0.0;
-                    if (in0) {
-                        const double W = inL ? sm.x[js][sidx - 1] : 0.0;
-                        const double ax = W + x3b + x4a + x2a - (dc0 + dr) * x3a;
+                    if (cg.in0) {
+                        const double W = cg.inL ? row[sidx - 1] : 0.0;
+                        const double ax = W + x3b + x4a + x2a - (cg.dc0 + dr3) * x3a;
                         ra = b3a - ax;
                         mx = max_drop_nan(mx, fabs(ra));
                         nan |= (ra != ra);
                         sx = sx + x3a;
                     }
-                    if (in1) {
-                        const double E = inR ? sm.x[js][sidx + 2] : 0.0;
-                        const double ax = x3a + E + x4b + x2b - (dc1 + dr) * x3b;
+                    if (cg.in1) {
+                        const double E = cg.inR ? row[sidx + 2] : 0.0;
+                        const double ax = x3a + E + x4b + x2b - (cg.dc1 + dr3) * x3b;
                         rb = b3b - ax;
                         mx = max_drop_nan(mx, fabs(rb));
                         nan |= (rb != rb);
                         sx = sx + x3b;
                     }
                     double* dst = xout + int64_t(j) * P.pitch + c0;
-                    if (in0 && in1) *reinterpret_cast<double2*>(dst) = make_double2(x3a, x3b);
-                    else if (in0) dst[0] = x3a;
+                    if (cg.in0 && cg.in1) *reinterpret_cast<double2*>(dst) = make_double2(x3a, x3b);
+                    else if (cg.in0) dst[0] = x3a;
                     tacc = tacc + (ra + rb);
                 }
-                if (j % P.tile == P.tile - 1 || j == P.ny - 1) {  // tile row-block complete
+                if ((j & tmask) == tmask || j == P.ny - 1) {  // tile row-block complete
                     if (t < kPairs) {
                         const double tsum = group_sum(tacc, g);
-                        if ((t % g) == 0 && in0) {
-                        P.cb.at(c0 / P.tile, j / P.tile) = tsum;
-                        cm = max_drop_nan(cm, fabs(tsum));
-                    }
+                        if ((t & (g - 1)) == 0 && cg.in0) {
+                            P.cb.at(c0 / P.tile, j / P.tile) = tsum;
+                            cm = max_drop_nan(cm, fabs(tsum));
+                        }
                     }
                     tacc = 0.0;
                 }
@@ -268,12 +291,17 @@ __device__ void sweep_body(Smem& sm, const Params& P, const Ctl& st) {
         // rotate the register window
         x4a = x3a, x4b = x3b, x3a = x2a, x3b = x2b, x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b;
         b3a = b2a, b3b = b2b, b2a = b1a, b2b = b1b, b1a = b0a, b1b = b0b;
+        dr3 = dr2, dr2 = dr1, dr1 = dr0;
+        // one barrier per row: iteration k+1 reads what iteration k wrote, and
+        // rows <= k-3 are free, so the slot of row k + kAheadSweep can refill
+        __syncthreads();
+        if (t == kProducer && k + kAheadSweep <= klast) issue_row(sm, P, xin, b, k + kAheadSweep, a, ncopy);
     }
     pass_epilogue(sm, P, kFine, mx, sx, cm, nan);
 }
 
 // ---- PROLONG / RESID body: x' = x + c + P ce, residual, restriction ---------
-__device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prolong) {
+__device__ __forceinline__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prolong) {
     const int a = blockIdx.x * kW;
     const int r0 = blockIdx.y * P.H, r1 = min(r0 + P.H, P.ny);
     const double* xin = st.buf[st.cur];
@@ -281,56 +309,53 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
     const double* b = st.b;
     const bool shift_on = st.has_shift != 0;
     const double c = st.shift;
-
-    const int t = threadIdx.x;
-    const bool owned = t < kPairs;
-    const bool halo = (t == kPairs) || (t == kPairs + 1);
-    const bool active = owned || halo;
-    const int c0 = owned ? a + 2 * t : (t == kPairs ? a - 2 : a + kW);
-    const int sidx = c0 - (a - 4);
-    const bool in0 = active && c0 >= 0 && c0 < P.nx, in1 = active && c0 + 1 >= 0 && c0 + 1 < P.nx;
-    const bool inL = active && c0 - 1 >= 0 && c0 - 1 < P.nx, inR = active && c0 + 2 < P.nx && c0 + 2 >= 0;
-    const double dc0 = col_diag(P, c0), dc1 = col_diag(P, c0 + 1);
+    const ColGeom cg(P, a);
+    const int t = cg.t, sidx = cg.sidx, c0 = cg.c0;
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    const double fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     const uint32_t ncopy = uint32_t(((min(a + kW + 4, P.nx + 5) - (a - 4)) + 1) & ~1);
+    const int tmask = P.tile - 1;
     // prolongation geometry of this thread's columns (TileAxis::locate_cell)
     int I0a = 0, I1a = 0, I0b = 0, I1b = 0;
     double sa = 0, dxa = 1, sb = 0, dxb = 1;
     if (prolong) {
-        if (in0) I0a = P.ax.k0[c0], I1a = P.ax.k1[c0], sa = P.ax.t[c0], dxa = P.ax.dk[c0];
-        if (in1) I0b = P.ax.k0[c0 + 1], I1b = P.ax.k1[c0 + 1], sb = P.ax.t[c0 + 1], dxb = P.ax.dk[c0 + 1];
+        if (cg.in0) I0a = P.ax.k0[c0], I1a = P.ax.k1[c0], sa = P.ax.t[c0], dxa = P.ax.dk[c0];
+        if (cg.in1) I0b = P.ax.k0[c0 + 1], I1b = P.ax.k1[c0 + 1], sb = P.ax.t[c0 + 1], dxb = P.ax.dk[c0 + 1];
     }
 
-    if (t == 0) {
+    if (t == kProducer) {
         for (int s = 0; s < kRing; ++s) mbar_init(&sm.bar[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     const int kfirst = r0 - 1, klast = r1;
-    if (t == 0)
+    if (t == kProducer)
         for (int k = kfirst; k <= min(klast, kfirst + kAheadRes - 1); ++k) issue_row(sm, P, xin, b, k, a, ncopy);
 
     double x0a = 0, x0b = 0, x1a = 0, x1b = 0, x2a = 0, x2b = 0, b0a = 0, b0b = 0, b1a = 0, b1b = 0;
+    double dr0 = 0, dr1 = 0;
     double mx = 0.0, sx = 0.0, tacc = 0.0, cm = 0.0;
     int nan = 0;
     const int g = P.tile >> 1;
     for (int k = kfirst; k <= klast; ++k) {
-        const int slot = (k + 2 * kRing) % kRing;
-        const uint32_t parity = uint32_t(((k - kfirst) / kRing) & 1);
-        mbar_wait(&sm.bar[slot], parity);
+        const int slot = k & (kRing - 1);
+        const uint32_t parity = (uint32_t(k - kfirst) >> 3) & 1u;  // fill count of this slot, mod 2
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), parity);
         const bool rk = k >= 0 && k < P.ny;
-        if (active) {
+        dr0 = ((k > 0) ? 1.0 : fwS) + ((k < P.ny - 1) ? 1.0 : fwN);  // row part of smoother.hpp:60-61
+        if (cg.active) {
             const double2 xv = *reinterpret_cast<const double2*>(&sm.x[slot][sidx]);
             const double2 bv = *reinterpret_cast<const double2*>(&sm.b[slot][sidx]);
-            double va = (rk && in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
-            double vb = (rk && in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
+            double va = (rk && cg.in0) ? (shift_on ? xv.x + c : xv.x) : 0.0;
+            double vb = (rk && cg.in1) ? (shift_on ? xv.y + c : xv.y) : 0.0;
             if (prolong && rk) {  // coarsening.hpp:495-500
                 const double tt = P.ay.t[k], dy = P.ay.dk[k];
                 const int J0 = P.ay.k0[k], J1 = P.ay.k1[k];
-                if (in0)
+                if (cg.in0)
                     va += ((dxa - sa) * ((dy - tt) * P.ce.at(I0a, J0) + tt * P.ce.at(I0a, J1)) +
                            sa * ((dy - tt) * P.ce.at(I1a, J0) + tt * P.ce.at(I1a, J1))) /
                           (dxa * dy);
-                if (in1)
+                if (cg.in1)
                     vb += ((dxb - sb) * ((dy - tt) * P.ce.at(I0b, J0) + tt * P.ce.at(I0b, J1)) +
                            sb * ((dy - tt) * P.ce.at(I1b, J0) + tt * P.ce.at(I1b, J1))) /
                           (dxb * dy);
@@ -340,24 +365,23 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
             *reinterpret_cast<double2*>(&sm.x[slot][sidx]) = make_double2(va, vb);
         }
         __syncthreads();
-        if (t == 0 && k + kAheadRes <= klast) issue_row(sm, P, xin, b, k + kAheadRes, a, ncopy);
+        if (t == kProducer && k + kAheadRes <= klast) issue_row(sm, P, xin, b, k + kAheadRes, a, ncopy);
         const int j = k - 1;
         if (j >= r0 && j < r1) {
-            if (owned) {
-                const int js = (j + 2 * kRing) % kRing;
-                const double dr = row_diag(P, j);
+            if (cg.owned) {
+                const double* row = sm.x[j & (kRing - 1)];
                 double ra = 0.0, rb = 0.0;
-                if (in0) {
-                    const double W = inL ? sm.x[js][sidx - 1] : 0.0;
-                    const double ax = W + x1b + x2a + x0a - (dc0 + dr) * x1a;
+                if (cg.in0) {
+                    const double W = cg.inL ? row[sidx - 1] : 0.0;
+                    const double ax = W + x1b + x2a + x0a - (cg.dc0 + dr1) * x1a;
                     ra = b1a - ax;
                     mx = max_drop_nan(mx, fabs(ra));
                     nan |= (ra != ra);
                     sx = sx + x1a;
                 }
-                if (in1) {
-                    const double E = inR ? sm.x[js][sidx + 2] : 0.0;
-                    const double ax = x1a + E + x2b + x0b - (dc1 + dr) * x1b;
+                if (cg.in1) {
+                    const double E = cg.inR ? row[sidx + 2] : 0.0;
+                    const double ax = x1a + E + x2b + x0b - (cg.dc1 + dr1) * x1b;
                     rb = b1b - ax;
                     mx = max_drop_nan(mx, fabs(rb));
                     nan |= (rb != rb);
@@ -365,15 +389,15 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
                 }
                 if (prolong) {
                     double* dst = xout + int64_t(j) * P.pitch + c0;
-                    if (in0 && in1) *reinterpret_cast<double2*>(dst) = make_double2(x1a, x1b);
-                    else if (in0) dst[0] = x1a;
+                    if (cg.in0 && cg.in1) *reinterpret_cast<double2*>(dst) = make_double2(x1a, x1b);
+                    else if (cg.in0) dst[0] = x1a;
                 }
                 tacc = tacc + (ra + rb);
             }
-            if (j % P.tile == P.tile - 1 || j == P.ny - 1) {
+            if ((j & tmask) == tmask || j == P.ny - 1) {
                 if (t < kPairs) {
                     const double tsum = group_sum(tacc, g);
-                    if ((t % g) == 0 && in0) {
+                    if ((t & (g - 1)) == 0 && cg.in0) {
                         P.cb.at(c0 / P.tile, j / P.tile) = tsum;
                         cm = max_drop_nan(cm, fabs(tsum));
                     }
@@ -382,18 +406,19 @@ __device__ void prolong_body(Smem& sm, const Params& P, const Ctl& st, bool prol
             }
         }
         x2a = x1a, x2b = x1b, x1a = x0a, x1b = x0b, b1a = b0a, b1b = b0b;
+        dr1 = dr0;
     }
     pass_epilogue(sm, P, prolong ? kProlong : kResid, mx, sx, cm, nan);
 }
 
 __global__ void __launch_bounds__(kThreads) fine_pass_kernel(Params P) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
+    __shared__ __align__(128) Smem sm;  // static: every ring access is an LDS/STS
+    const Ctl st = *P.ctl;              // snapshot (written only by the previous kernel)
     if (st.phase == kFine) sweep_body(sm, P, st);
     else if (st.phase == kProlong) prolong_body(sm, P, st, true);
     else if (st.phase == kResid) prolong_body(sm, P, st, false);
 }
+
 // final anchor + copy into the caller's field: x = buf[cur] + c
 __global__ void finalize_kernel(Params P, View xuser) {
     const Ctl* s = P.ctl;
@@ -407,14 +432,9 @@ __global__ void finalize_kernel(Params P, View xuser) {
     xuser.at(i, j) = sh ? v + c : v;
 }
 
-
-void launch_fine_pass(const Params& P, dim3 grid, size_t smem, cudaStream_t st) {
-    fine_pass_kernel<<<grid, kThreads, smem, st>>>(P);
-}
-size_t fine_pass_smem() { return sizeof(Smem); }
-void set_fine_pass_smem(size_t bytes) {
-    ISMG_CUDA(cudaFuncSetAttribute(fine_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-}
+void launch_fine_pass(const Params& P, dim3 grid, size_t, cudaStream_t st) { fine_pass_kernel<<<grid, kThreads, 0, st>>>(P); }
+size_t fine_pass_smem() { return 0; }  // static shared memory (sizeof(Smem) < 48 KB)
+void set_fine_pass_smem(size_t) {}
 void launch_finalize(const Params& P, View xuser, cudaStream_t st) {
     finalize_kernel<<<dim3((P.nx + 255) / 256, P.ny), 256, 0, st>>>(P, xuser);
 }
