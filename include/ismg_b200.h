@@ -146,6 +146,7 @@ typedef struct ismg_solve_stats {
     double fine_pass_ms;        /* summed CUDA-event time of fine passes      */
     double coarse_ms;           /* summed CUDA-event time of coarse visits    */
     double solve_ms;            /* CUDA-event time of the whole solve         */
+    int64_t coarse_steps;       /* wavefront steps of the coarse visits       */
 } ismg_solve_stats;
 
 /* ---- opaque handles ------------------------------------------------------ */

@@ -103,6 +103,7 @@ class CSolveStats(C.Structure):
         ("fine_pass_ms", C.c_double),
         ("coarse_ms", C.c_double),
         ("solve_ms", C.c_double),
+        ("coarse_steps", C.c_int64),
     ]
 
 

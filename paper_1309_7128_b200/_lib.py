@@ -10,7 +10,7 @@ import os
 from ._abi import (CCycleConfig, CGridSpec, CReport, CSolveStats, CStepMetrics, DP, I32P)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libismg_b200.so")
+LIB_PATH = os.environ.get("ISMG_LIB") or os.path.join(HERE, "libismg_b200.so")  # ISMG_LIB: experiment builds
 
 _lib = None
 

@@ -336,11 +336,14 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
     __shared__ TmSmem cs;
     Ctl* st = P.ctl;
     if (st->phase != kCoarse) return;
+    const long long t_start = gtimer();
+    long long steps = 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3, h = warp >> 2;
     const int J = 32 * q + lane;
     const bool rowok = J < T.ncy;
     const int ncx = T.ncx, ncy = T.ncy, PP = T.PP;
+    const int dmax = (ncx - 1) + 2 * (ncy - 1);
     const int nxs = (ncy + 2) * T.pitch;
     double* xs = dyn;
     double* spec = dyn + max(nxs, ncx * ncy);
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
         if (G > 1)
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) backup[k] = xs[k];  // checkpoint
         tm_group<Kind, kTmU>(T, xs, spec, tq, cs, G, true);
+        steps += dmax + kLagT * (G - 1) + 5;
         if (threadIdx.x == 0) {
             int first = -1;
             double rg = 0.0;
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) xs[k] = backup[k];
             __syncthreads();
             tm_group<Kind, kTmU>(T, xs, spec, tq, cs, first + 1, false);
+            steps += dmax + kLagT * first + 1;
             done += first + 1;
             break;
         }
@@ -434,6 +439,8 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(cs.tmem_base));
     if (threadIdx.x == 0) {
         st->coarse_launches += 1;
+        st->coarse_ns += gtimer() - t_start;
+        st->coarse_steps += steps;
         if (done > 0) st->pred = int(done);
         st->total += done;
         st->coarse += done;

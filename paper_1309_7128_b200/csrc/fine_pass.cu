@@ -23,104 +23,6 @@
 namespace ismgb {
 namespace fz {
 
-// ---- per-CTA epilogue + control flow (last CTA) ------------------------------
-__device__ __forceinline__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
-    Ctl* s = P.ctl;
-    s->passes += 1;
-    s->r = r;
-    if (P.singular) {  // anchor after every residual check (field.hpp:49,53-59)
-        s->shift = -(sum / P.ncells);
-        s->has_shift = 1;
-    }
-    if (mode != kResid) s->cur ^= 1;
-    if (s->hold) return;  // ismg_bench_fine_pass: repeat the same pass kind
-    auto to_coarse = [&]() {
-        s->restrictions += 1;
-        if (s->nvisits < P.visit_cap) {
-            P.visit_log[2 * s->nvisits] = 0;
-            P.visit_log[2 * s->nvisits + 1] = 0;
-        }
-        s->nvisits += 1;
-        s->rc = rc0;
-        if (rc0 > P.tol_coarse) {
-            s->phase = kCoarse;
-        } else {  // zero-sweep visit: no prolongation, relax again (cycles.hpp:125,138,146)
-            s->prev = r;
-            s->phase = kFine;
-        }
-    };
-    if (mode == kFine) {  // cycles.hpp:147-161
-        s->total += 1;
-        s->fine += 1;
-        if (s->nvisits > 0 && s->nvisits <= P.visit_cap) P.visit_log[2 * (s->nvisits - 1) + 1] += 1;
-        if (r <= P.tol_fine) {
-            s->phase = kDone, s->converged = 1;
-        } else if (s->total >= P.max_total) {
-            s->phase = kDone, s->converged = 0;
-        } else if (r > P.stall * s->prev) {
-            to_coarse();
-        } else {
-            s->prev = r;
-            s->phase = kFine;
-        }
-    } else if (mode == kProlong) {  // cycles.hpp:138-146
-        s->prolongations += 1;
-        if (r <= P.tol_fine) {
-            s->phase = kDone, s->converged = 1;
-        } else {
-            s->prev = r;
-            if (s->total >= P.max_total) s->phase = kDone, s->converged = 0;
-            else s->phase = kFine;
-        }
-    } else {  // initial residual, cycles.hpp:111-118
-        if (r <= P.tol_fine) {
-            s->phase = kDone, s->converged = 1;
-        } else if (s->total >= P.max_total) {
-            s->phase = kDone, s->converged = 0;
-        } else {
-            to_coarse();
-        }
-    }
-}
-
-// cm = max |tile sum| this CTA wrote to cb: the coarse entry residual
-// coarse_residual(ce = 0, cb) = max|cb| (cycles.hpp:122-123) is complete when
-// the pass ends, so a visit that needs no coarse sweep is decided here.
-__device__ __forceinline__ void pass_epilogue(Smem& sm, const Params& P, int mode, double mx, double sx, double cm, int nan) {
-    const int nb = gridDim.x * gridDim.y;
-    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-    double bm = block_max(mx, sm.red[0]);
-    double bs = block_sum(sx, sm.red[1]);
-    double bc = block_max(cm, sm.red[2]);
-    int anynan = __syncthreads_or(nan);
-    if (threadIdx.x == 0) {
-        P.part[3 * bid] = bm;
-        P.part[3 * bid + 1] = bs;
-        P.part[3 * bid + 2] = bc;
-        if (anynan) P.ctl->nan_seen = 1;
-        __threadfence();
-        const unsigned t = atomicAdd(P.ticket, 1u);
-        sm.last = (t == unsigned(nb - 1));
-    }
-    __syncthreads();
-    if (!sm.last) return;
-    __threadfence();
-    double m = 0.0, s = 0.0, c = 0.0;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-        m = fmax(m, __ldcg(&P.part[3 * k]));
-        s += __ldcg(&P.part[3 * k + 1]);
-        c = fmax(c, __ldcg(&P.part[3 * k + 2]));
-    }
-    m = block_max(m, sm.red[0]);
-    s = block_sum(s, sm.red[1]);
-    c = block_max(c, sm.red[2]);
-    if (threadIdx.x == 0) {
-        fine_decide(P, mode, m, s, c);
-        *P.ticket = 0u;
-        __threadfence();
-    }
-}
-
 // ---- SWEEP body: anchor-shift, red, black, residual, restriction ------------
 // ---- per-thread column geometry -------------------------------------------
 // Threads 0..kPairs-1 own the column pairs (a + 2t, a + 2t + 1) of the strip;
@@ -259,16 +161,14 @@ __device__ __forceinline__ void sweep_body(Smem& sm, const Params& P, const Ctl&
                         const double W = cg.inL ? row[sidx - 1] : 0.0;
                         const double ax = W + x3b + x4a + x2a - (cg.dc0 + dr3) * x3a;
                         ra = b3a - ax;
-                        mx = max_drop_nan(mx, fabs(ra));
-                        nan |= (ra != ra);
+                        mx = fmax(mx, fabs(ra));  // fmax drops NaN, as std::max(rmax, |r|) does
                         sx = sx + x3a;
                     }
                     if (cg.in1) {
                         const double E = cg.inR ? row[sidx + 2] : 0.0;
                         const double ax = x3a + E + x4b + x2b - (cg.dc1 + dr3) * x3b;
                         rb = b3b - ax;
-                        mx = max_drop_nan(mx, fabs(rb));
-                        nan |= (rb != rb);
+                        mx = fmax(mx, fabs(rb));
                         sx = sx + x3b;
                     }
                     double* dst = xout + int64_t(j) * P.pitch + c0;
@@ -282,6 +182,7 @@ __device__ __forceinline__ void sweep_body(Smem& sm, const Params& P, const Ctl&
                         if ((t & (g - 1)) == 0 && cg.in0) {
                             P.cb.at(c0 / P.tile, j / P.tile) = tsum;
                             cm = max_drop_nan(cm, fabs(tsum));
+                            nan |= (tsum != tsum);  // a NaN residual poisons its tile sum
                         }
                     }
                     tacc = 0.0;
@@ -375,16 +276,14 @@ __device__ __forceinline__ void prolong_body(Smem& sm, const Params& P, const Ct
                     const double W = cg.inL ? row[sidx - 1] : 0.0;
                     const double ax = W + x1b + x2a + x0a - (cg.dc0 + dr1) * x1a;
                     ra = b1a - ax;
-                    mx = max_drop_nan(mx, fabs(ra));
-                    nan |= (ra != ra);
+                    mx = fmax(mx, fabs(ra));  // fmax drops NaN, as std::max(rmax, |r|) does
                     sx = sx + x1a;
                 }
                 if (cg.in1) {
                     const double E = cg.inR ? row[sidx + 2] : 0.0;
                     const double ax = x1a + E + x2b + x0b - (cg.dc1 + dr1) * x1b;
                     rb = b1b - ax;
-                    mx = max_drop_nan(mx, fabs(rb));
-                    nan |= (rb != rb);
+                    mx = fmax(mx, fabs(rb));
                     sx = sx + x1b;
                 }
                 if (prolong) {
@@ -400,6 +299,7 @@ __device__ __forceinline__ void prolong_body(Smem& sm, const Params& P, const Ct
                     if ((t & (g - 1)) == 0 && cg.in0) {
                         P.cb.at(c0 / P.tile, j / P.tile) = tsum;
                         cm = max_drop_nan(cm, fabs(tsum));
+                        nan |= (tsum != tsum);  // a NaN residual poisons its tile sum
                     }
                 }
                 tacc = 0.0;

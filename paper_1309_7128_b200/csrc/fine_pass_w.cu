@@ -1,0 +1,478 @@
+// fine_pass_w.cu — the fused fine pass on independent one-warp strips (tiles >= 4).
+//
+// Same pass as fine_pass.cu (anchor shift, red and black half-sweeps,
+// residual, tile-sum restriction, anchor sum and max|r| in ONE HBM pass of
+// 24 B/cell). Measured on B200, the pass is bound by the latency of each
+// warp's in-order dependent instruction stream and by its slowest warps, so:
+//   * a CTA is ONE warp owning a strip of nq column quads (lanes 1..nq;
+//     4*nq a multiple of the tile, <= 120 columns); lanes 0 and nq+1 hold the
+//     halo quads (a-4..a-1, a+4nq..a+4nq+3) and recompute the 2/1-cell
+//     red / black halo; a finished strip frees its SM slot at once;
+//   * the warp streams rows through its own shared-memory ring filled by TMA
+//     bulk copies (issued from converged code by an elected lane) and
+//     exchanges horizontal neighbours with shuffles; there is no CTA barrier;
+//   * iteration k loads row k, relaxes the red cells of row k-1, the black
+//     cells of row k-2 and forms the residual of row k-3 (vertical
+//     neighbours in registers, slots compile-time in a 4-row unroll);
+//   * every warp runs the SAME arithmetic: cells are relaxed with d = 4, and
+//     boundary cases are fix-ups behind branches taken only where they apply:
+//     lanes holding a boundary or out-of-domain column (lane-divergent, rare)
+//     and boundary rows (warp-uniform). Out-of-domain lanes stay frozen at 0,
+//     which is exactly the missing neighbour of the reference's stencil, so
+//     boundary strips cost what interior strips cost.
+#include <type_traits>
+
+#include "fused_impl.cuh"
+
+namespace ismgb {
+namespace fz {
+
+namespace {
+
+constexpr int kRowW = 128;  // ring row: columns [a-4, a+124)
+constexpr int kRingW = 6;   // rows in flight
+
+struct SmemW {
+    double x[kRingW][kRowW];
+    double b[kRingW][kRowW];
+    uint64_t bar[kRingW];
+};
+
+// TMA bulk copies of one row (x and b) into ring slot `slot`: called by the
+// whole converged warp; one elected lane issues.
+__device__ __forceinline__ void issue_row_w(SmemW& sm, const double* xrow, const double* brow, int slot,
+                                            uint32_t bytes) {
+    const uint32_t bar = su32(&sm.bar[slot]);
+    const uint32_t dx = su32(&sm.x[slot][0]), db = su32(&sm.b[slot][0]);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%5], [%6], %4, [%0];\n\t"
+        "}" ::"r"(bar),
+        "r"(2u * bytes), "r"(dx), "l"(xrow), "r"(bytes), "r"(db), "l"(brow)
+        : "memory");
+}
+
+// Per-lane column geometry.
+struct Lane {
+    int l, c0;
+    bool owned;   // lanes 1..nq: residual, store, tile sums
+    bool frozen;  // no column of the lane in the domain (idle lanes, outside halos): values stay 0
+    bool spec;    // a boundary column or a partly outside quad: exact per-cell fix-up
+    bool dom[4], red[4], blk[4];
+    double dc[4];  // column part of the diagonal (W + E faces)
+    __device__ __forceinline__ Lane(const Params& P, int a, int nq) {
+        l = threadIdx.x & 31;
+        owned = l >= 1 && l <= nq;
+        const bool active = l <= nq + 1;
+        c0 = a - 4 + 4 * l;
+        const int W = 4 * nq;
+        bool any = false, all = true, interior = true;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = c0 + q;
+            dom[q] = active && col >= 0 && col < P.nx;
+            any = any || dom[q];
+            all = all && dom[q];
+            interior = interior && col >= 1 && col <= P.nx - 2;
+            red[q] = dom[q] && col >= a - 2 && col < a + W + 2;
+            blk[q] = dom[q] && col >= a - 1 && col < a + W + 1;
+            dc[q] = col_diag(P, col);
+        }
+        frozen = !any;
+        owned = owned && any;  // a quad entirely past the last column stores and sums nothing
+        spec = any && !(all && interior);
+    }
+};
+
+struct Acc {
+    double mx = 0.0, sx = 0.0, tacc = 0.0, cm = 0.0;
+    int nan = 0;
+};
+
+// Register window: at the top of iteration k (U = its index in a 4-row
+// block) rows k-1, k-2, k-3, k-4 live in slots (U+3)&3, (U+2)&3, (U+1)&3, U.
+struct Win {
+    double x[4][4];
+    double b[4][4];
+};
+
+struct Geo {
+    int r0, r1, ny;
+    double c, fwS, fwN;
+    double* outp;
+    int64_t pitch;
+};
+
+__device__ __forceinline__ double row_part(const Geo& G, int j) {
+    return ((j > 0) ? 1.0 : G.fwS) + ((j < G.ny - 1) ? 1.0 : G.fwN);  // smoother.hpp:60-61
+}
+
+__device__ __forceinline__ double sh_up(double v) { return __shfl_up_sync(kFull, v, 1); }
+__device__ __forceinline__ double sh_dn(double v) { return __shfl_down_sync(kFull, v, 1); }
+
+// Exact update of one cell (smoother.hpp:112-113) for the fix-up paths.
+__device__ __forceinline__ double gs_exact(double W, double E, double S, double N, double b, double d) {
+    return div_by_diag(((((W + E) + S) + N) - b), d);
+}
+
+// Iteration k; row k-1 has parity P1.
+template <int U, int P1>
+__device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L, const Geo& G, Win& w, Acc& A, int k) {
+    constexpr int s0 = U, s1 = (U + 3) & 3, s2 = (U + 2) & 3, s3 = (U + 1) & 3;
+    const int si = 4 * L.l;
+    double t[4];
+    {
+        const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+        t[0] = v01.x + G.c, t[1] = v01.y + G.c, t[2] = v23.x + G.c, t[3] = v23.y + G.c;
+        if (k < 0 || k >= G.ny || L.frozen) {  // rows outside the domain / frozen lanes hold 0
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[q] = 0.0;
+        } else if (L.spec) {  // columns outside the domain hold 0
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[q] = L.dom[q] ? t[q] : 0.0;
+        }
+        w.b[s0][0] = b01.x, w.b[s0][1] = b01.y, w.b[s0][2] = b23.x, w.b[s0][3] = b23.y;
+#ifdef ISMG_DBG
+        if (blockIdx.x == 0 && blockIdx.y == 1 && (L.l == 5 || L.l == 25) && k <= G.r0 + 3)
+            printf("load k=%d U=%d slot=%d lane=%d raw=%g t=%g\n", k, U, slot, L.l, v01.x, t[0]);
+#endif
+    }
+    double* x1 = w.x[s1];
+    double* x2 = w.x[s2];
+    double* x3 = w.x[s3];
+    const double* x4 = w.x[s0];  // row k-4
+    // neighbour exchanges (inputs final before this iteration)
+    const double redW = sh_up(x1[3]), redE = sh_dn(x1[0]);  // raw black edges of row k-1
+    const double blkW = sh_up(x2[3]), blkE = sh_dn(x2[0]);  // red edges of row k-2
+    const double resW = sh_up(x3[3]), resE = sh_dn(x3[0]);  // final edges of row k-3
+    // ---- red half-sweep of row j = k-1 (red cells: col + j even; S = row k-2, N = row k)
+    {
+        const int j = k - 1;
+        if (j >= G.r0 - 2 && j >= 0 && j < G.ny) {
+            const double* b = w.b[s1];
+            constexpr int qa = P1, qb = qa + 2;
+            const double Wa = qa == 0 ? redW : x1[0], Ea = x1[qa + 1];
+            const double Wb = x1[qb - 1], Eb = qb == 3 ? redE : x1[3];
+            double va = ((((Wa + Ea) + x2[qa]) + t[qa]) - b[qa]) * 0.25;
+            double vb = ((((Wb + Eb) + x2[qb]) + t[qb]) - b[qb]) * 0.25;
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                va = L.red[qa] ? gs_exact(Wa, Ea, x2[qa], t[qa], b[qa], L.dc[qa] + dr) : x1[qa];
+                vb = L.red[qb] ? gs_exact(Wb, Eb, x2[qb], t[qb], b[qb], L.dc[qb] + dr) : x1[qb];
+            }
+            if (!L.frozen) x1[qa] = va, x1[qb] = vb;
+        }
+    }
+    // ---- black half-sweep of row j = k-2 (parity 1 - P1; S = row k-3, N = row k-1 relaxed)
+    {
+        const int j = k - 2;
+        if (j >= G.r0 - 1 && j >= 0 && j < G.ny) {
+            const double* b = w.b[s2];
+            // black cells of row k-2 ((col + j) odd) sit in the columns of row k-1's red cells
+            constexpr int qa = P1, qb = qa + 2;
+            const double Wa = qa == 0 ? blkW : x2[0], Ea = x2[qa + 1];
+            const double Wb = x2[qb - 1], Eb = qb == 3 ? blkE : x2[3];
+            double va = ((((Wa + Ea) + x3[qa]) + x1[qa]) - b[qa]) * 0.25;
+            double vb = ((((Wb + Eb) + x3[qb]) + x1[qb]) - b[qb]) * 0.25;
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                va = L.blk[qa] ? gs_exact(Wa, Ea, x3[qa], x1[qa], b[qa], L.dc[qa] + dr) : x2[qa];
+                vb = L.blk[qb] ? gs_exact(Wb, Eb, x3[qb], x1[qb], b[qb], L.dc[qb] + dr) : x2[qb];
+            }
+            if (!L.frozen) x2[qa] = va, x2[qb] = vb;
+        }
+    }
+    // ---- residual of row j = k-3 (smoother.hpp:121-141) and store
+    {
+        const int j = k - 3;
+        if (j >= G.r0 && j < G.r1 && L.owned) {
+            const double* b = w.b[s3];
+            double r[4];
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                r[0] = b[0] - ((((resW + x3[1]) + x4[0]) + x2[0]) - (L.dc[0] + dr) * x3[0]);
+                r[1] = b[1] - ((((x3[0] + x3[2]) + x4[1]) + x2[1]) - (L.dc[1] + dr) * x3[1]);
+                r[2] = b[2] - ((((x3[1] + x3[3]) + x4[2]) + x2[2]) - (L.dc[2] + dr) * x3[2]);
+                r[3] = b[3] - ((((x3[2] + resE) + x4[3]) + x2[3]) - (L.dc[3] + dr) * x3[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            } else {
+                r[0] = b[0] - ((((resW + x3[1]) + x4[0]) + x2[0]) - 4.0 * x3[0]);
+                r[1] = b[1] - ((((x3[0] + x3[2]) + x4[1]) + x2[1]) - 4.0 * x3[1]);
+                r[2] = b[2] - ((((x3[1] + x3[3]) + x4[2]) + x2[2]) - 4.0 * x3[2]);
+                r[3] = b[3] - ((((x3[2] + resE) + x4[3]) + x2[3]) - 4.0 * x3[3]);
+            }
+            const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
+            A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));  // std::max(rmax, |r|): NaN dropped
+            A.sx = A.sx + ((x3[0] + x3[1]) + (x3[2] + x3[3]));   // out-of-domain cells hold 0
+            A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
+            double* dst = G.outp + int64_t(j) * G.pitch;
+#ifdef ISMG_DBG
+            if (blockIdx.x == 0 && blockIdx.y == 1 && (L.l == 5 || L.l == 25) && j <= G.r0 + 1)
+                printf("res k=%d j=%d lane=%d x3=%g x4=%g x2=%g b=%g dst=%p\n", k, j, L.l, x3[0], x4[0], x2[0], b[0], dst);
+#endif
+            if (!L.spec) {
+                reinterpret_cast<double2*>(dst)[0] = make_double2(x3[0], x3[1]);
+                reinterpret_cast<double2*>(dst)[1] = make_double2(x3[2], x3[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (L.dom[q]) dst[q] = x3[q];
+            }
+        }
+    }
+    // row k takes the slot of row k-4
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w.x[s0][q] = t[q];
+}
+
+// tile row-block complete: fold the g = tile/4 lanes of every coarse cell
+// (groups start at lane 1; the tile is a power of two)
+__device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int j, int lg, Acc& A) {
+    const int g = P.tile >> 2;
+    double v = A.tacc;
+    for (int o = g >> 1; o > 0; o >>= 1) v = v + __shfl_down_sync(kFull, v, o);
+    if (L.owned && ((L.l - 1) & (g - 1)) == 0 && L.dom[0]) {
+        P.cb.at(L.c0 >> lg, j >> lg) = v;
+        A.cm = max_drop_nan(A.cm, fabs(v));
+        A.nan |= (v != v);  // a NaN residual poisons its tile sum
+    }
+    A.tacc = 0.0;
+}
+
+// Warp-level epilogue: one partial triple per warp (= CTA); the last warp to
+// finish reduces them and applies the reference's branch logic.
+__device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double mx, double sx, double cm, int nan) {
+    const int nb = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    mx = warp_max(mx);
+    sx = warp_sum_down(sx);
+    cm = warp_max(cm);
+    const int anynan = __any_sync(kFull, nan);
+    unsigned last = 0;
+    if ((threadIdx.x & 31) == 0) {
+        P.part[3 * bid] = mx;
+        P.part[3 * bid + 1] = sx;
+        P.part[3 * bid + 2] = cm;
+        if (anynan) P.ctl->nan_seen = 1;
+        __threadfence();
+        last = atomicAdd(P.ticket, 1u) == unsigned(nb - 1);
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (!last) return;
+    __threadfence();
+    double m = 0.0, s = 0.0, c = 0.0;
+    for (int k = threadIdx.x & 31; k < nb; k += 32) {
+        m = fmax(m, __ldcg(&P.part[3 * k]));
+        s += __ldcg(&P.part[3 * k + 1]);
+        c = fmax(c, __ldcg(&P.part[3 * k + 2]));
+    }
+    m = warp_max(m);
+    s = warp_sum_down(s);
+    c = warp_max(c);
+    if ((threadIdx.x & 31) == 0) {
+        fine_decide(P, mode, m, s, c);
+        *P.ticket = 0u;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
+
+__device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& st, int nq) {
+    const int W = 4 * nq;
+    const int a = blockIdx.x * W;
+    const Lane L(P, a, nq);
+    Geo G;
+    G.r0 = blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.ny), G.ny = P.ny;
+    G.c = st.has_shift ? st.shift : -0.0;  // x + (-0.0) == x for every x
+    G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
+    G.outp = st.buf[st.cur ^ 1] + L.c0;
+    G.pitch = P.pitch;
+    const int tmask = P.tile - 1, lg = ilog2(P.tile);
+    const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
+    const double* xrow0 = st.buf[st.cur] + (a - 4);
+    const double* brow0 = st.b + (a - 4);
+    const int kfirst = G.r0 - 3, klast = G.r1 + 2;
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
+        issue_row_w(sm, xrow0 + int64_t(kfirst + s) * G.pitch, brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+    Win w;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w.x[s][q] = w.b[s][q] = 0.0;
+    Acc A;
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    int slot = 0;
+    uint32_t phase = 0;
+    auto row = [&](auto u, int k) {
+        constexpr int U = decltype(u)::value;
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
+        step_w<U, (U & 1)>(sm, slot, L, G, w, A, k);
+        const int j = k - 3;  // tile row-block of row k-3 complete
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
+        __syncwarp();  // every lane has read the slot of row k
+        if (k + kRingW <= klast)
+            issue_row_w(sm, xrow0 + int64_t(k + kRingW) * G.pitch, brow0 + int64_t(k + kRingW) * G.pitch, slot,
+                        bytes);
+        if (++slot == kRingW) slot = 0, phase ^= 1u;
+    };
+    // kfirst = r0 - 3 = 1 (mod 4) (P.H is a multiple of 4), so in the block
+    // starting at kb the row k-1 = kb - 1 + U has the parity of U
+    for (int kb = kfirst; kb <= klast; kb += 4) {
+        row(std::integral_constant<int, 0>{}, kb);
+        if (kb + 1 <= klast) row(std::integral_constant<int, 1>{}, kb + 1);
+        if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, kb + 2);
+        if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, kb + 3);
+    }
+    warp_epilogue(P, kFine, A.mx, A.sx, A.cm, A.nan);
+}
+
+// ---- PROLONG / RESID: x' = x + c + P ce (coarsening.hpp:495-500), residual and
+// restriction of x'. Iteration k loads (and prolongs) row k and forms the
+// residual of row k-1 with rows k-2, k-1 in registers.
+__device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl& st, int nq, bool prolong) {
+    const int W = 4 * nq;
+    const int a = blockIdx.x * W;
+    const Lane L(P, a, nq);
+    Geo G;
+    G.r0 = blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.ny), G.ny = P.ny;
+    G.c = st.has_shift ? st.shift : -0.0;
+    G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
+    G.outp = st.buf[st.cur ^ 1] + L.c0;
+    G.pitch = P.pitch;
+    const int tmask = P.tile - 1, lg = ilog2(P.tile);
+    const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
+    const double* xrow0 = st.buf[st.cur] + (a - 4);
+    const double* brow0 = st.b + (a - 4);
+    Acc A;
+    // TileAxis::locate_cell of the lane's columns
+    int I0[4], I1[4];
+    double sq[4], dxq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        I0[q] = I1[q] = 0, sq[q] = 0.0, dxq[q] = 1.0;
+        if (prolong && L.dom[q]) {
+            const int col = L.c0 + q;
+            I0[q] = P.ax.k0[col], I1[q] = P.ax.k1[col], sq[q] = P.ax.t[col], dxq[q] = P.ax.dk[col];
+        }
+    }
+    const int kfirst = G.r0 - 1, klast = G.r1;
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
+        issue_row_w(sm, xrow0 + int64_t(kfirst + s) * G.pitch, brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    double x1[4] = {0, 0, 0, 0}, x2[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
+    int slot = 0;
+    uint32_t phase = 0;
+    const int si = 4 * L.l;
+    for (int k = kfirst; k <= klast; ++k) {
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
+        double x0[4], b0[4];
+        {
+            const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
+            const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
+            const double2 c01 = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+            const double2 c23 = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+            const double raw[4] = {v01.x, v01.y, v23.x, v23.y};
+            b0[0] = c01.x, b0[1] = c01.y, b0[2] = c23.x, b0[3] = c23.y;
+            const bool rin = k >= 0 && k < G.ny;
+            double tt = 0.0, dy = 1.0;
+            int J0 = 0, J1 = 0;
+            if (prolong && rin) tt = P.ay.t[k], dy = P.ay.dk[k], J0 = P.ay.k0[k], J1 = P.ay.k1[k];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double v = (rin && L.dom[q]) ? raw[q] + G.c : 0.0;
+                if (prolong && rin && L.dom[q]) {
+                    const double num =
+                        (dxq[q] - sq[q]) * ((dy - tt) * P.ce.at(I0[q], J0) + tt * P.ce.at(I0[q], J1)) +
+                        sq[q] * ((dy - tt) * P.ce.at(I1[q], J0) + tt * P.ce.at(I1[q], J1));
+                    const double den = dxq[q] * dy;
+                    // a power-of-two den (uniform tiles): the reciprocal product is the exact quotient
+                    const bool pow2 = (__double_as_longlong(den) & 0x000FFFFFFFFFFFFFll) == 0;
+                    v += pow2 ? num * (1.0 / den) : num / den;
+                }
+                x0[q] = v;
+            }
+        }
+        const double W1 = sh_up(x1[3]), E1 = sh_dn(x1[0]);
+        const int j = k - 1;
+        if (L.owned && j >= G.r0 && j < G.r1) {
+            const double dr = row_part(G, j);
+            double r[4];
+            r[0] = b1[0] - ((((W1 + x1[1]) + x2[0]) + x0[0]) - (L.dc[0] + dr) * x1[0]);
+            r[1] = b1[1] - ((((x1[0] + x1[2]) + x2[1]) + x0[1]) - (L.dc[1] + dr) * x1[1]);
+            r[2] = b1[2] - ((((x1[1] + x1[3]) + x2[2]) + x0[2]) - (L.dc[2] + dr) * x1[2]);
+            r[3] = b1[3] - ((((x1[2] + E1) + x2[3]) + x0[3]) - (L.dc[3] + dr) * x1[3]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
+            A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
+            A.sx = A.sx + ((x1[0] + x1[1]) + (x1[2] + x1[3]));
+            A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
+            if (prolong) {
+                double* dst = G.outp + int64_t(j) * G.pitch;
+                if (!L.spec) {
+                    reinterpret_cast<double2*>(dst)[0] = make_double2(x1[0], x1[1]);
+                    reinterpret_cast<double2*>(dst)[1] = make_double2(x1[2], x1[3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (L.dom[q]) dst[q] = x1[q];
+                }
+            }
+        }
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x2[q] = x1[q], x1[q] = x0[q], b1[q] = b0[q];
+        __syncwarp();
+        if (k + kRingW <= klast)
+            issue_row_w(sm, xrow0 + int64_t(k + kRingW) * G.pitch, brow0 + int64_t(k + kRingW) * G.pitch, slot,
+                        bytes);
+        if (++slot == kRingW) slot = 0, phase ^= 1u;
+    }
+    warp_epilogue(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan);
+}
+
+__global__ void __launch_bounds__(32) fine_pass_w_kernel(Params P, int nq) {
+    __shared__ __align__(128) SmemW sm;
+    const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
+    if (st.phase == kFine) sweep_w(sm, P, st, nq);
+    else if (st.phase == kProlong) prolong_w(sm, P, st, nq, true);
+    else if (st.phase == kResid) prolong_w(sm, P, st, nq, false);
+}
+
+}  // namespace
+
+// owned quads per warp: the most tile-aligned quads that fit 30 lanes
+int fine_pass_w_quads(int tile) {
+    const int g = tile / 4;
+    return (30 / g) * g;
+}
+size_t fine_pass_w_smem() { return 0; }  // static shared memory
+void set_fine_pass_w_smem() {}
+dim3 fine_pass_w_grid(const Params& P) {
+    const int W = 4 * fine_pass_w_quads(P.tile);
+    return dim3((P.nx + W - 1) / W, P.nchunks);
+}
+void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st) {
+    fine_pass_w_kernel<<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
+}
+
+}  // namespace fz
+}  // namespace ismgb

@@ -27,6 +27,7 @@ struct FusedEngine {
     double* tm_spec = nullptr;
     int graph_slots = 0;
     size_t smem = 0;
+    int fine_kind = 0;  // 0 column pairs (256-column CTA strips), 2 one-warp strips of column quads
     dim3 grid;
     cudaEvent_t ev = nullptr;
 };
@@ -43,6 +44,11 @@ bool fused_supported(const Solver& s) {
     return true;
 }
 
+static void launch_fine(const FusedEngine& e, cudaStream_t st) {
+    if (e.fine_kind == 2) launch_fine_pass_w(e.P, e.grid, st);
+    else launch_fine_pass(e.P, e.grid, e.smem, st);
+}
+
 static void capture_graph(FusedEngine& e, int slots) {
     Ctx& c = *e.s->ctx;
     if (e.graph) cudaGraphExecDestroy(e.graph);
@@ -56,7 +62,7 @@ static void capture_graph(FusedEngine& e, int slots) {
             launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
         else
             launch_coarse_global(e.P, c.stream);
-        launch_fine_pass(e.P, e.grid, e.smem, c.stream);
+        launch_fine(e, c.stream);
     }
     ISMG_CUDA(cudaStreamEndCapture(c.stream, &g));
     ISMG_CUDA(cudaGraphInstantiate(&e.graph, g, 0));
@@ -73,8 +79,19 @@ FusedEngine* make_fused(Solver& s) {
     Params& P = e->P;
     P.nx = s.g.nx, P.ny = s.g.ny, P.pitch = e->scratch.pitch;
     P.tile = s.g.tile, P.ncx = L.h.ncx, P.ncy = L.h.ncy;
-    P.H = std::max(P.tile, 128 / P.tile * P.tile);
-    P.nstrips = (P.nx + kW - 1) / kW;
+    // fine kernel: one-warp strips of column quads when a tile spans >= 4 columns
+    // (test hook ISMG_FINE_KERNEL=pair forces the column-pair kernel)
+    const char* fk = getenv("ISMG_FINE_KERNEL");
+    e->fine_kind = (P.tile >= 4) ? 2 : 0;
+    if (fk && std::string(fk) == "pair") e->fine_kind = 0;
+    const int width = e->fine_kind == 2 ? 4 * fine_pass_w_quads(P.tile) : kW;
+    // rows per CTA chunk: one-warp strips want many short chunks (more resident warps)
+    P.H = e->fine_kind == 2 ? std::max(P.tile, 32) : std::max(P.tile, 128 / P.tile * P.tile);
+    if (const char* h = getenv("ISMG_FINE_H")) {  // tuning hook: rows per CTA chunk (rounded to tiles)
+        const int v = atoi(h);
+        if (v > 0) P.H = std::max(P.tile, v / P.tile * P.tile);
+    }
+    P.nstrips = (P.nx + width - 1) / width;
     P.nchunks = (P.ny + P.H - 1) / P.H;
     P.bc = s.bc;
     P.singular = s.singular ? 1 : 0;
@@ -97,8 +114,14 @@ FusedEngine* make_fused(Solver& s) {
     ISMG_CUDA(cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
     P.ctl = e->d_ctl;
     e->grid = dim3(P.nstrips, P.nchunks);
-    e->smem = fine_pass_smem();
-    set_fine_pass_smem(e->smem);
+    if (e->fine_kind == 2) {
+        e->grid = fine_pass_w_grid(P);
+        e->smem = fine_pass_w_smem();
+        set_fine_pass_w_smem();
+    } else {
+        e->smem = fine_pass_smem();
+        set_fine_pass_smem(e->smem);
+    }
     ISMG_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
     // coarse-visit kernel: TMEM-resident rhs when the operator allows it,
     // else shared-memory iterate, else the global-memory wavefront
@@ -159,7 +182,7 @@ double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters) {
     for (auto& v : ev) ISMG_CUDA(cudaEventCreate(&v));
     ISMG_CUDA(cudaEventRecord(ev[0], c.stream));
     for (int k = 0; k < iters; ++k) {
-        launch_fine_pass(e.P, e.grid, e.smem, c.stream);
+        launch_fine(e, c.stream);
         ISMG_CUDA(cudaEventRecord(ev[size_t(k) + 1], c.stream));
     }
     c.launches += iters;
@@ -241,6 +264,8 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.fine_passes = st.fine;
     s.last.prolong_passes = st.prolongations;
     s.last.coarse_visits = st.coarse_launches;
+    s.last.coarse_ms = double(st.coarse_ns) * 1e-6;
+    s.last.coarse_steps = st.coarse_steps;
     s.last.kernel_launches = 2 * launched_slots + 2;
 }
 

@@ -33,6 +33,7 @@ struct Ctl {
     int pred;  // predicted coarse-visit length (sweeps of the previous visit)
     long long total, fine, coarse, restrictions, prolongations;
     long long passes, coarse_launches;
+    long long coarse_ns, coarse_steps;  // device-timed coarse visits (globaltimer) and their wavefront steps
     double r, prev, shift, rc;
     double* buf[2];
     const double* b;
@@ -57,6 +58,12 @@ struct Params {
     int visit_cap;
     double* coarse_scratch;  // reduction scratch for the coarse kernel
 };
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---- PTX helpers: mbarrier + TMA bulk copy ----------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -107,7 +114,9 @@ struct Smem {
 __device__ __forceinline__ void issue_row(Smem& sm, const Params& P, const double* xin, const double* b, int row,
                                           int a, uint32_t ncopy) {
     const int slot = (row + 2 * kRing) % kRing;  // row may be -3
+#ifdef ISMG_PROXY_FENCE
     fence_proxy_async();
+#endif
     mbar_expect_tx(&sm.bar[slot], 2u * ncopy * 8u);
     const int64_t off = int64_t(row) * P.pitch + (a - 4);
     bulk_load(sm.x[slot], xin + off, ncopy * 8u, &sm.bar[slot]);
@@ -129,10 +138,116 @@ __device__ __forceinline__ double group_sum(double v, int g) {
     return v;
 }
 
+// ---- per-CTA epilogue + control flow (last CTA) ------------------------------
+__device__ __forceinline__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
+    Ctl* s = P.ctl;
+    s->passes += 1;
+    s->r = r;
+    if (P.singular) {  // anchor after every residual check (field.hpp:49,53-59)
+        s->shift = -(sum / P.ncells);
+        s->has_shift = 1;
+    }
+    if (mode != kResid) s->cur ^= 1;
+    if (s->hold) return;  // ismg_bench_fine_pass: repeat the same pass kind
+    auto to_coarse = [&]() {
+        s->restrictions += 1;
+        if (s->nvisits < P.visit_cap) {
+            P.visit_log[2 * s->nvisits] = 0;
+            P.visit_log[2 * s->nvisits + 1] = 0;
+        }
+        s->nvisits += 1;
+        s->rc = rc0;
+        if (rc0 > P.tol_coarse) {
+            s->phase = kCoarse;
+        } else {  // zero-sweep visit: no prolongation, relax again (cycles.hpp:125,138,146)
+            s->prev = r;
+            s->phase = kFine;
+        }
+    };
+    if (mode == kFine) {  // cycles.hpp:147-161
+        s->total += 1;
+        s->fine += 1;
+        if (s->nvisits > 0 && s->nvisits <= P.visit_cap) P.visit_log[2 * (s->nvisits - 1) + 1] += 1;
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else if (s->total >= P.max_total) {
+            s->phase = kDone, s->converged = 0;
+        } else if (r > P.stall * s->prev) {
+            to_coarse();
+        } else {
+            s->prev = r;
+            s->phase = kFine;
+        }
+    } else if (mode == kProlong) {  // cycles.hpp:138-146
+        s->prolongations += 1;
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else {
+            s->prev = r;
+            if (s->total >= P.max_total) s->phase = kDone, s->converged = 0;
+            else s->phase = kFine;
+        }
+    } else {  // initial residual, cycles.hpp:111-118
+        if (r <= P.tol_fine) {
+            s->phase = kDone, s->converged = 1;
+        } else if (s->total >= P.max_total) {
+            s->phase = kDone, s->converged = 0;
+        } else {
+            to_coarse();
+        }
+    }
+}
+
+// cm = max |tile sum| this CTA wrote to cb: the coarse entry residual
+// coarse_residual(ce = 0, cb) = max|cb| (cycles.hpp:122-123) is complete when
+// the pass ends, so a visit that needs no coarse sweep is decided here.
+template <class S>
+__device__ __noinline__ void pass_epilogue(S& sm, const Params& P, int mode, double mx, double sx, double cm, int nan) {
+    const int nb = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    double bm = block_max(mx, sm.red[0]);
+    double bs = block_sum(sx, sm.red[1]);
+    double bc = block_max(cm, sm.red[2]);
+    int anynan = __syncthreads_or(nan);
+    if (threadIdx.x == 0) {
+        P.part[3 * bid] = bm;
+        P.part[3 * bid + 1] = bs;
+        P.part[3 * bid + 2] = bc;
+        if (anynan) P.ctl->nan_seen = 1;
+        __threadfence();
+        const unsigned t = atomicAdd(P.ticket, 1u);
+        sm.last = (t == unsigned(nb - 1));
+    }
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    double m = 0.0, s = 0.0, c = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        m = fmax(m, __ldcg(&P.part[3 * k]));
+        s += __ldcg(&P.part[3 * k + 1]);
+        c = fmax(c, __ldcg(&P.part[3 * k + 2]));
+    }
+    m = block_max(m, sm.red[0]);
+    s = block_sum(s, sm.red[1]);
+    c = block_max(c, sm.red[2]);
+    if (threadIdx.x == 0) {
+        fine_decide(P, mode, m, s, c);
+        *P.ticket = 0u;
+        __threadfence();
+    }
+}
+
+
 // launchers (each in the translation unit of its kernel)
 void launch_fine_pass(const Params& P, dim3 grid, size_t smem, cudaStream_t st);
 size_t fine_pass_smem();
 void set_fine_pass_smem(size_t bytes);
+// independent warp strips (fine_pass_w.cu; tiles >= 4)
+int fine_pass_w_quads(int tile);
+size_t fine_pass_w_smem();
+void set_fine_pass_w_smem();
+dim3 fine_pass_w_grid(const Params& P);
+void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st);
 void launch_finalize(const Params& P, View xuser, cudaStream_t st);
 void launch_coarse_global(const Params& P, cudaStream_t st);
 void launch_coarse_smem(const Params& P, double* backup, size_t smem, cudaStream_t st);

@@ -13,4 +13,6 @@ ds = P.DeviceState(case.grid, solver.ctx, st)
 m = RunMetrics(n * n)
 ds.step(solver, m)
 s = solver.last_stats()
-print("solve %.1f ms, I_f %d I_c %d, visits %s" % (s["solve_ms"], m.rows[-1].fine_sweeps, m.rows[-1].coarse_sweeps, solver.visit_log()[:4]))
+print("solve %.1f ms, coarse %.1f ms over %d wavefront steps (%.2f us/step), I_f %d I_c %d, visits %s"
+      % (s["solve_ms"], s["coarse_ms"], s["coarse_steps"], 1e3 * s["coarse_ms"] / max(1, s["coarse_steps"]),
+         m.rows[-1].fine_sweeps, m.rows[-1].coarse_sweeps, solver.visit_log()[:4]))
