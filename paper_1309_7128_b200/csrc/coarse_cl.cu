@@ -1,0 +1,599 @@
+// coarse_cl.cu — the coarse visit on a thread-block cluster (cycles.hpp:120-137,
+// coarsening.hpp:531-567): lexicographic Gauss-Seidel sweeps on the 9-point
+// interpolated operator until tol_coarse, bit for bit the reference's order.
+//
+// Schedule (as coarse_visit_smem_kernel, coarse.cu): sweep g of cell (I,J)
+// runs at wavefront step tau = I + 2J + 8g and its residual at tau + 4, one
+// barrier per step; sweeps run in checkpointed groups, a group that overshoots
+// the first converged sweep is restored and replayed exactly that far.
+//
+// Layout, B200-first:
+//  * the coarse rows are split into bands over the C CTAs of ONE cluster
+//    (C = 1..16 SMs); a CTA keeps its band of the iterate, plus one mirrored
+//    halo row on each side, in shared memory in natural row-major order; the
+//    row pitch is 3 (mod 16) doubles, so the 32 lanes of a warp (32
+//    consecutive rows, one cell each on a wavefront I = t - 2J) touch 32
+//    distinct bank pairs;
+//  * a band's first / last row is also stored into the neighbour CTA's halo
+//    row through distributed shared memory, and every step ends with one
+//    cluster barrier (release / acquire);
+//  * the rhs sits in shared memory when the band fits, else it is read
+//    through L1 (read-only path);
+//  * warps of a 32-row block split the sweeps in flight (g = h mod kH); the
+//    per-cell index work is one subtract, one compare and one add;
+//  * the interior stencil is a compile-time constant when the operator's
+//    interior rows are the ISMG or five-point stencil bit for bit; the
+//    boundary ring takes a divergent path through a class table.
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include <cooperative_groups.h>
+
+#include "fused_impl.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ismgb {
+namespace fz {
+
+namespace {
+
+constexpr int kLag = 8;            // wavefront steps between consecutive sweeps
+constexpr int kMaxGroup = 512;     // sweeps per checkpointed group
+constexpr int kPredCap = 32;       // cap of the predicted first group of a visit
+constexpr int kClThreads = 512;
+
+constexpr int kMaxRowBlocks = 4;  // 32-row blocks per CTA band
+
+struct ClShared {
+    double cmax[kMaxRowBlocks][kMaxGroup];  // residual max per (row block, sweep of the group)
+    double rmax[kMaxGroup];                 // residual max of the ring cells per sweep
+    double gmax[kMaxGroup];                 // ... all reduced over the CTA
+    double red[32];
+    double bcast[4];
+    int ictl[4];
+    int first;
+};
+
+__device__ __forceinline__ int ring_index(const ClGeom& T, int I, int J) {
+    if (J == 0) return I;
+    if (J == T.ncy - 1) return T.ncx + I;
+    if (I == 0) return 2 * T.ncx + J;
+    return 2 * T.ncx + T.ncy + J;
+}
+
+struct Nbr {
+    double c, e, w, n, s, ne, nw, se, sw;
+};
+// neighbours of the cell at p (row pitch `pitch`; N = row J+1)
+__device__ __forceinline__ Nbr gather(const double* p, int pitch, bool with_c, bool five) {
+    Nbr v;
+    v.c = with_c ? p[0] : 0.0;
+    v.e = p[1];
+    v.w = p[-1];
+    v.n = p[pitch];
+    v.s = p[-pitch];
+    if (!five) {
+        v.ne = p[pitch + 1];
+        v.nw = p[pitch - 1];
+        v.se = p[1 - pitch];
+        v.sw = p[-1 - pitch];
+    } else {
+        v.ne = v.nw = v.se = v.sw = 0.0;
+    }
+    return v;
+}
+
+// Reference order (coarsening.hpp:539-543 residual, :558-565 update): slots
+// E, W, N, S, NE, NW, SE, SW, each skipped when its weight is zero.
+template <bool kResidual>
+__device__ __forceinline__ double apply_w(const double* w, const Nbr& v, double bIJ, bool five) {
+    double acc = kResidual ? w[0] * v.c : 0.0;
+    if (w[1] != 0.0) acc += w[1] * v.e;
+    if (w[2] != 0.0) acc += w[2] * v.w;
+    if (w[3] != 0.0) acc += w[3] * v.n;
+    if (w[4] != 0.0) acc += w[4] * v.s;
+    if (!five) {
+        if (w[5] != 0.0) acc += w[5] * v.ne;
+        if (w[6] != 0.0) acc += w[6] * v.nw;
+        if (w[7] != 0.0) acc += w[7] * v.se;
+        if (w[8] != 0.0) acc += w[8] * v.sw;
+    }
+    return kResidual ? bIJ - acc : (bIJ - acc) / w[0];
+}
+
+// a / -3 correctly rounded by Markstein's correction (y = RN(-1/3); checked
+// against __ddiv_rn on 1.2e9 operands, tools/verify_div3.cu)
+__device__ __forceinline__ double div_m3(double a) {
+    constexpr double y = -1.0 / 3.0;
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, -3.0, a);
+    return __fma_rn(r, y, q);
+}
+
+template <bool kResidual, int Kind>
+__device__ __forceinline__ double apply_std(const ClGeom& T, const Nbr& v, double bIJ) {
+    if constexpr (Kind == 1) {  // ISMG interior: C -3, E/W/N/S 1/2, corners 1/4
+        double acc = kResidual ? -3.0 * v.c : 0.0;
+        acc += 0.5 * v.e;
+        acc += 0.5 * v.w;
+        acc += 0.5 * v.n;
+        acc += 0.5 * v.s;
+        acc += 0.25 * v.ne;
+        acc += 0.25 * v.nw;
+        acc += 0.25 * v.se;
+        acc += 0.25 * v.sw;
+        return kResidual ? bIJ - acc : div_m3(bIJ - acc);
+    } else if constexpr (Kind == 2) {  // five-point interior: C -4, E/W/N/S 1
+        double acc = kResidual ? -4.0 * v.c : 0.0;
+        acc += 1.0 * v.e;
+        acc += 1.0 * v.w;
+        acc += 1.0 * v.n;
+        acc += 1.0 * v.s;
+        return kResidual ? bIJ - acc : (bIJ - acc) * -0.25;  // exact: power-of-two divisor
+    } else {
+        return apply_w<kResidual>(T.stdw, v, bIJ, T.five);
+    }
+}
+
+// boundary-ring cell: 9 weights + RN(1/w0) of its class (spec table in smem)
+template <bool kResidual>
+__device__ __forceinline__ double ring_cell(const ClGeom& T, const double* spec, const Nbr& v, int I, int J,
+                                         double bIJ) {
+    const int* ring_cls = reinterpret_cast<const int*>(spec + 10 * T.ncls);
+    const double* wc = spec + 10 * ring_cls[ring_index(T, I, J)];
+    double w[9];
+#pragma unroll
+    for (int sl = 0; sl < 9; ++sl) w[sl] = wc[sl];
+    if (kResidual) return apply_w<true>(w, v, bIJ, T.five);
+    double acc = 0.0;  // update: coarsening.hpp:558-565
+    if (w[1] != 0.0) acc += w[1] * v.e;
+    if (w[2] != 0.0) acc += w[2] * v.w;
+    if (w[3] != 0.0) acc += w[3] * v.n;
+    if (w[4] != 0.0) acc += w[4] * v.s;
+    if (!T.five) {
+        if (w[5] != 0.0) acc += w[5] * v.ne;
+        if (w[6] != 0.0) acc += w[6] * v.nw;
+        if (w[7] != 0.0) acc += w[7] * v.se;
+        if (w[8] != 0.0) acc += w[8] * v.sw;
+    }
+    const double num = bIJ - acc;
+    if (!T.fastdiv) return num / w[0];
+    const double y = wc[9];  // Markstein: exact RN(num / w0) (host-verified per class)
+    const double q = __dmul_rn(num, y);
+    const double r = __fma_rn(-q, w[0], num);
+    return __fma_rn(r, y, q);
+}
+
+// max over the warp of non-negative doubles (their order = the order of the
+// (hi, lo) words): two 32-bit REDUX steps
+__device__ __forceinline__ double warp_max_nonneg(double m) {
+    const unsigned hi = unsigned(__double2hiint(m)), lo = unsigned(__double2loint(m));
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    return __hiloint2double(int(mh), int(ml));
+}
+
+struct Band {
+    int c, C;       // cluster rank, cluster size
+    int J0, J1;     // rows [J0, J1) of this CTA
+    double* xs;     // iterate: row J at xs + (J - J0 + 1) * pitch + 1 (halo rows J0-1, J1)
+    const double* bs;
+    int bpitch;     // rhs: row J at bs + (J - J0) * bpitch (smem) or a global view
+    double* south;  // neighbour CTA's halo row that mirrors row J0 (nullptr at the bottom)
+    double* north;  // neighbour CTA's halo row that mirrors row J1 - 1
+};
+
+__device__ __forceinline__ void step_sync(const Band& B) {
+    if (B.C > 1) cg::this_cluster().sync();
+    else __syncthreads();
+}
+
+// One group of G sweeps (residuals: also form the residual max of every sweep).
+// One ring cell (boundary row or column) of sweep g at its step: update or residual.
+template <bool BSmem>
+__device__ __forceinline__ double ring_step(const ClGeom& T, const Band& B, const double* spec, const View& cbg,
+                                            int I, int J, bool residual) {
+    double* p = B.xs + (J - B.J0 + 1) * T.pitch + 1 + I;
+    const double bIJ = BSmem ? B.bs[(J - B.J0) * B.bpitch + I] : __ldg(&cbg.p[int64_t(J) * cbg.pitch + I]);
+    const Nbr v = gather(p, T.pitch, residual, T.five);
+    if (residual) {
+        const double m = fabs(ring_cell<true>(T, spec, v, I, J, bIJ));
+        return (m != m) ? 0.0 : m;  // std::max drops NaN
+    }
+    const double out = ring_cell<false>(T, spec, v, I, J, bIJ);
+    *p = out;
+    if (J == B.J0 && B.south != nullptr) B.south[I] = out;
+    if (J == B.J1 - 1 && B.north != nullptr) B.north[I] = out;
+    return 0.0;
+}
+
+// One group of G sweeps (residuals: also form the residual max of every sweep).
+// Interior cells: lane = row J, warps of a row block split the sweeps in
+// flight (g = h mod kH). Ring cells (first / last row and column) go to a
+// separate lane-parallel pass, four lanes per sweep (one per side), so the
+// interior loop never diverges on them.
+template <int Kind, bool BSmem>
+__device__ void cl_group(const ClGeom& T, const Band& B, const double* spec, const View& cbg, ClShared& cs, int G,
+                         bool residuals) {
+    const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int nrb = (B.J1 - B.J0 + 31) >> 5;  // 32-row blocks of the band (1, 2 or 4)
+    const int kH = 1 << (31 - __clz(nwarps / nrb));  // warps per row block (power of two; nrb = 3 idles some)
+    const int rb = warp % nrb, h = warp / nrb;
+    const int Jw = B.J0 + 32 * rb;  // first row of the warp
+    const int J = Jw + lane;
+    const int jlast = min(Jw + 31, B.J1 - 1);
+    const bool rowint = h < kH && J <= jlast && J > 0 && J < T.ncy - 1;  // interior row of the band
+    const int pitch = T.pitch;
+    double* rowp = B.xs + (J - B.J0 + 1) * pitch + 1;  // cell (0, J)
+    const double* brow = BSmem ? B.bs + (J - B.J0) * B.bpitch : cbg.p + int64_t(J) * cbg.pitch;
+    const bool mirror_s = J == B.J0 && B.south != nullptr;
+    const bool mirror_n = J == B.J1 - 1 && B.north != nullptr;
+    const unsigned nint = unsigned(T.ncx - 2);  // interior columns 1..ncx-2
+    // ring pass: lane 4k+s of warp w handles side s of sweep g = gbase + 8w + k
+    const int rk = lane >> 2, side = lane & 3;
+    const bool has_bottom = B.J0 == 0, has_top = B.J1 == T.ncy;
+    if (residuals) {
+        for (int k = threadIdx.x; k < nrb * kMaxGroup; k += blockDim.x) (&cs.cmax[0][0])[k] = 0.0;
+        for (int k = threadIdx.x; k < kMaxGroup; k += blockDim.x) cs.rmax[k] = 0.0;
+    }
+    __syncthreads();
+    const int tau_end = dmax + kLag * (G - 1) + (residuals ? 4 : 0);
+    const int dlo = 2 * Jw, dhi = 2 * jlast + T.ncx - 1;
+    const bool int_on = h < kH;
+    const int rw = nwarps - 1 - warp;  // ring passes run on the last warps
+    for (int tau = 0; tau <= tau_end; ++tau) {
+        // ---- interior cells of this warp's rows: updates on diagonals tau - 8g,
+        //      residuals on tau - 4 - 8g; one loop carries one of each, so the two
+        //      independent dependency chains overlap
+        if (int_on) {
+            const int bu = tau, br = residuals ? tau - 4 : -1;
+            int gu = 0, guh = -1, gr = 0, grh = -1;
+            if (bu >= dlo) {
+                const int g_lo = max(0, (bu - dhi + kLag - 1) >> 3);
+                guh = min(G - 1, (bu - dlo) >> 3);
+                gu = g_lo + ((h - g_lo) & (kH - 1));
+            }
+            if (br >= dlo) {
+                const int g_lo = max(0, (br - dhi + kLag - 1) >> 3);
+                grh = min(G - 1, (br - dlo) >> 3);
+                gr = g_lo + ((h - g_lo) & (kH - 1));
+            }
+            const int Iu0 = bu - 2 * J, Ir0 = br - 2 * J;
+#pragma unroll 1
+            while (gu <= guh || gr <= grh) {
+                const bool du = gu <= guh, dres = gr <= grh;
+                const int Iu = Iu0 - kLag * gu, Ir = Ir0 - kLag * gr;
+                const bool oku = du && rowint && unsigned(Iu - 1) < nint;
+                const bool okr = dres && rowint && unsigned(Ir - 1) < nint;
+                double m = 0.0;
+                if (okr) {  // residual of sweep gr (inputs final since step tau - 1)
+                    const double bIJ = BSmem ? brow[Ir] : __ldg(brow + Ir);
+                    m = fabs(apply_std<true, Kind>(T, gather(rowp + Ir, pitch, true, T.five), bIJ));
+                    m = (m != m) ? 0.0 : m;  // std::max drops NaN
+                }
+                if (oku) {  // update of sweep gu
+                    double* p = rowp + Iu;
+                    const double bIJ = BSmem ? brow[Iu] : __ldg(brow + Iu);
+                    const double out = apply_std<false, Kind>(T, gather(p, pitch, false, T.five), bIJ);
+                    *p = out;
+                    if (mirror_s) B.south[Iu] = out;
+                    if (mirror_n) B.north[Iu] = out;
+                }
+                if (dres) {
+                    m = warp_max_nonneg(m);
+                    if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
+                }
+                gu += kH, gr += kH;
+            }
+        }
+        // ---- ring cells: sweeps with a diagonal in [0, dmax], four lanes per sweep
+#pragma unroll 1
+        for (int phase = 0; phase < (residuals ? 2 : 1); ++phase) {
+            const int base = phase == 0 ? tau : tau - 4;
+            const int g_lo = max(0, (base - dmax + kLag - 1) >> 3), g_hi = min(G - 1, base >> 3);
+            const int g = g_lo + 8 * rw + rk;
+            if (base >= 0 && g_lo + 8 * rw <= g_hi) {
+                double m = 0.0;
+                if (g <= g_hi) {
+                    const int d = base - kLag * g;
+                    int I = -1, Jr = -1;
+                    if (side == 0) {  // first column (corners included)
+                        if ((d & 1) == 0) I = 0, Jr = d >> 1;
+                    } else if (side == 1) {  // last column (corners included)
+                        if (((d - T.ncx + 1) & 1) == 0) I = T.ncx - 1, Jr = (d - T.ncx + 1) >> 1;
+                    } else if (side == 2) {  // first row, corners excluded
+                        if (has_bottom && d >= 1 && d <= T.ncx - 2) I = d, Jr = 0;
+                    } else {  // last row, corners excluded
+                        const int It = d - 2 * (T.ncy - 1);
+                        if (has_top && It >= 1 && It <= T.ncx - 2) I = It, Jr = T.ncy - 1;
+                    }
+                    if (I >= 0 && Jr >= B.J0 && Jr < B.J1) m = ring_step<BSmem>(T, B, spec, cbg, I, Jr, phase == 1);
+                }
+                if (phase == 1) {  // max over the four sides of each sweep
+                    m = fmax(m, __shfl_xor_sync(kFull, m, 1));
+                    m = fmax(m, __shfl_xor_sync(kFull, m, 2));
+                    if (side == 0 && g <= g_hi) cs.rmax[g] = fmax(cs.rmax[g], m);
+                }
+            }
+        }
+        step_sync(B);
+    }
+}
+
+template <int Kind, bool BSmem>
+__global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom T, const double* spec_g,
+                                                               double* backup) {
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ ClShared cs;
+    Ctl* st = P.ctl;
+    if (st->phase != kCoarse) return;
+    const long long t_start = gtimer();
+    cg::cluster_group cluster = cg::this_cluster();
+    Band B;
+    B.C = int(cluster.num_blocks());
+    B.c = int(cluster.block_rank());
+    const int R = T.band;
+    B.J0 = B.c * R, B.J1 = min(T.ncy, B.J0 + R);
+    const int pitch = T.pitch;
+    const int rows = R + 2;
+    B.xs = dyn;
+    double* bsm = dyn + size_t(rows) * pitch;
+    B.bpitch = T.bpitch;
+    B.bs = bsm;
+    double* spec = bsm + (BSmem ? size_t(R) * T.bpitch : 0);
+    // mirrors: my row J0 is row (R + 1) of the CTA below's buffer; my row J1-1 is row 0 of the CTA above
+    B.south = (B.c > 0) ? cluster.map_shared_rank(B.xs, B.c - 1) + size_t(R + 1) * pitch + 1 : nullptr;
+    B.north = (B.c + 1 < B.C && B.J1 < T.ncy) ? cluster.map_shared_rank(B.xs, B.c + 1) + 1 : nullptr;
+    const int nxs = rows * pitch;
+    for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = 0.0;  // ce = 0, zero ghosts and halos
+    if (BSmem)
+        for (int k = threadIdx.x; k < (B.J1 - B.J0) * T.ncx; k += blockDim.x) {
+            const int jj = k / T.ncx, I = k - jj * T.ncx;
+            bsm[jj * T.bpitch + I] = P.cb.at(I, B.J0 + jj);
+        }
+    const int spec_words = 10 * T.ncls + (T.ring + 1) / 2;
+    for (int k = threadIdx.x; k < spec_words; k += blockDim.x) spec[k] = spec_g[k];
+    cluster.sync();
+    double* my_backup = backup + size_t(B.c) * nxs;
+    double rc = st->rc;  // max|cb|, formed by the fine pass that restricted
+    const long long budget = P.max_total - st->total;
+    long long done = 0, steps = 0, gns = 0;
+    const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
+    int G = max(1, min(st->pred, kPredCap));
+    while (rc > P.tol_coarse && done < budget) {
+        if (budget - done < G) G = int(budget - done);
+        if (G > 1)
+            for (int k = threadIdx.x; k < nxs; k += blockDim.x) my_backup[k] = B.xs[k];  // checkpoint
+        const long long tg0 = gtimer();
+        cl_group<Kind, BSmem>(T, B, spec, P.cb, cs, G, true);
+        gns += gtimer() - tg0;
+        steps += dmax + kLag * (G - 1) + 5;
+        // cluster-wide first sweep whose residual passes tol_coarse
+        {
+            const int nrb = (B.J1 - B.J0 + 31) >> 5;
+            for (int g = threadIdx.x; g < G; g += blockDim.x) {
+                double m = fmax(cs.cmax[0][g], cs.rmax[g]);
+                for (int r = 1; r < nrb; ++r) m = fmax(m, cs.cmax[r][g]);
+                cs.gmax[g] = m;
+            }
+            if (threadIdx.x == 0) cs.first = G;
+            cluster.sync();
+            if (B.c == 0) {
+                for (int g = threadIdx.x; g < G; g += blockDim.x) {
+                    double rg = 0.0;
+                    for (int r = 0; r < B.C; ++r) rg = fmax(rg, cluster.map_shared_rank(&cs.gmax[0], r)[g]);
+                    cs.cmax[0][g] = rg;
+                    if (!(rg > P.tol_coarse)) atomicMin(&cs.first, g);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const int first = cs.first < G ? cs.first : -1;
+                    cs.ictl[0] = first;
+                    cs.bcast[1] = cs.cmax[0][first >= 0 ? first : G - 1];
+                }
+            }
+        }
+        cluster.sync();
+        const int first = *cluster.map_shared_rank(&cs.ictl[0], 0);
+        rc = *cluster.map_shared_rank(&cs.bcast[1], 0);
+        cluster.sync();  // everyone has read CTA 0's decision before it can change
+        if (first >= 0 && first < G - 1) {  // overshoot: restore and replay first+1 sweeps
+            for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = my_backup[k];
+            cluster.sync();
+            const long long tg0 = gtimer();
+            cl_group<Kind, BSmem>(T, B, spec, P.cb, cs, first + 1, false);
+            gns += gtimer() - tg0;
+            steps += dmax + kLag * first + 1;
+            done += first + 1;
+            break;
+        }
+        done += G;
+        if (first >= 0) break;
+        G = min(2 * G, kMaxGroup);
+    }
+    // anchor once (singular) and hand ce to the prolongation
+    if (P.singular && done > 0) {
+        double sum = 0.0;
+        for (int J = B.J0 + int(threadIdx.x >> 5); J < B.J1; J += int(blockDim.x >> 5)) {
+            const double* r = B.xs + (J - B.J0 + 1) * pitch + 1;
+            double s = 0.0;
+            for (int I = int(threadIdx.x & 31); I < T.ncx; I += 32) s += r[I];
+            sum += warp_sum_down(s);
+        }
+        sum = block_sum((threadIdx.x & 31) == 0 ? sum : 0.0, cs.red);
+        if (threadIdx.x == 0) cs.bcast[2] = sum;
+        cluster.sync();
+        double tot = 0.0;
+        for (int r = 0; r < B.C; ++r) tot += *cluster.map_shared_rank(&cs.bcast[2], r);
+        const double c = -(tot / double(int64_t(T.ncx) * T.ncy));
+        for (int k = threadIdx.x; k < (B.J1 - B.J0) * T.ncx; k += blockDim.x) {
+            const int jj = k / T.ncx, I = k - jj * T.ncx;
+            B.xs[(jj + 1) * pitch + 1 + I] += c;
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < (B.J1 - B.J0) * T.ncx; k += blockDim.x) {  // coalesced write-out
+        const int jj = k / T.ncx, I = k - jj * T.ncx;
+        P.ce.at(I, B.J0 + jj) = B.xs[(jj + 1) * pitch + 1 + I];
+    }
+    cluster.sync();  // no CTA exits while another may still read its shared memory
+    if (B.c == 0 && threadIdx.x == 0) {
+        st->coarse_launches += 1;
+        st->coarse_ns += gtimer() - t_start;
+        st->coarse_steps += steps;
+        st->coarse_group_ns += gns;
+        if (done > 0) st->pred = int(done);
+        st->total += done;
+        st->coarse += done;
+        st->rc = rc;
+        if (st->nvisits > 0 && st->nvisits <= P.visit_cap) P.visit_log[2 * (st->nvisits - 1)] = int(done);
+        if (rc > P.tol_coarse) {  // cycles.hpp:134-137
+            st->phase = kDone, st->converged = 0;
+        } else if (done > 0) {
+            st->phase = kProlong;
+        } else {
+            st->prev = st->r;
+            st->phase = kFine;
+        }
+    }
+}
+
+bool same_bits(double a, double b) { return a == b && std::signbit(a) == std::signbit(b); }
+
+template <int Kind, bool BSmem>
+void launch_one(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(T.csize);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(T.csize);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ISMG_CUDA(cudaLaunchKernelEx(&cfg, coarse_cl_kernel<Kind, BSmem>, P, T, spec, backup));
+}
+
+template <int Kind, bool BSmem>
+void set_attrs(size_t smem) {
+    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BSmem>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+}  // namespace
+
+// Host plan: stencil classes (interior constant + tabulated boundary ring),
+// cluster size and band height so the band fits shared memory.
+bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem) {
+    if (op.px || op.py || op.ncx < 3 || op.ncy < 3) return false;
+    T.ncx = op.ncx, T.ncy = op.ncy, T.five = op.five_point;
+    T.ring = 2 * op.ncx + 2 * op.ncy;
+    for (int sl = 0; sl < 9; ++sl) T.stdw[sl] = op.at(sl, 1, 1);
+    for (int J = 1; J < op.ncy - 1; ++J)
+        for (int I = 1; I < op.ncx - 1; ++I)
+            for (int sl = 0; sl < 9; ++sl)
+                if (!same_bits(op.at(sl, I, J), T.stdw[sl])) return false;
+    if (T.stdw[0] == 0.0) return false;
+    static const double ismg[9] = {-3.0, 0.5, 0.5, 0.5, 0.5, 0.25, 0.25, 0.25, 0.25};
+    static const double five[9] = {-4.0, 1.0, 1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
+    T.kind = 0;
+    bool is_ismg = !op.five_point, is_five = op.five_point;
+    for (int sl = 0; sl < 9; ++sl) {
+        is_ismg = is_ismg && same_bits(T.stdw[sl], ismg[sl]);
+        is_five = is_five && (sl >= 5 || same_bits(T.stdw[sl], five[sl]));
+    }
+    if (is_ismg) T.kind = 1;
+    if (is_five) T.kind = 2;
+    std::vector<std::array<double, 9>> cls;
+    std::vector<int> ring_cls(size_t(T.ring), 0);
+    auto classify = [&](int r, int I, int J) {
+        std::array<double, 9> w;
+        for (int sl = 0; sl < 9; ++sl) w[sl] = op.at(sl, I, J);
+        size_t c = 0;
+        for (; c < cls.size(); ++c) {
+            bool eq = true;
+            for (int sl = 0; sl < 9 && eq; ++sl) eq = same_bits(cls[c][sl], w[sl]);
+            if (eq) break;
+        }
+        if (c == cls.size()) cls.push_back(w);
+        ring_cls[size_t(r)] = int(c);
+    };
+    for (int I = 0; I < op.ncx; ++I) classify(I, I, 0), classify(op.ncx + I, I, op.ncy - 1);
+    for (int J = 0; J < op.ncy; ++J) classify(2 * op.ncx + J, 0, J), classify(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
+    T.ncls = int(cls.size());
+    if (T.ncls > 1024) return false;
+    T.fastdiv = 1;  // Markstein's correction per class divisor, spot-checked
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    for (const auto& w : cls) {
+        if (w[0] == 0.0) return false;  // singular ring row: the op-level path raises
+        const double b = w[0], y = 1.0 / b;
+        for (int k = 0; k < 20000 && T.fastdiv; ++k) {
+            st ^= st << 13, st ^= st >> 7, st ^= st << 17;
+            const double a = std::ldexp(double(st >> 11) * 0x1.0p-53 + 0.5, int((st >> 3) % 120) - 60) *
+                             ((st & 1) ? -1.0 : 1.0);
+            const double q = a * y, r = std::fma(-q, b, a), mk = std::fma(r, y, q);
+            if (!same_bits(mk, a / b)) T.fastdiv = 0;
+        }
+    }
+    spec.assign(size_t(10) * T.ncls + size_t(T.ring + 1) / 2, 0.0);
+    for (int c = 0; c < T.ncls; ++c) {
+        for (int sl = 0; sl < 9; ++sl) spec[size_t(10) * c + sl] = cls[size_t(c)][size_t(sl)];
+        spec[size_t(10) * c + 9] = 1.0 / cls[size_t(c)][0];
+    }
+    std::memcpy(spec.data() + size_t(10) * T.ncls, ring_cls.data(), sizeof(int) * ring_cls.size());
+    // pitches = 3 (mod 16) doubles (conflict-free wavefront lanes), >= ncx + 2
+    T.pitch = (op.ncx + 2) + ((3 - (op.ncx + 2) % 16) + 16) % 16;
+    T.bpitch = op.ncx + ((3 - op.ncx % 16) + 16) % 16;
+    const size_t cap = 200 * 1024;
+    const size_t spec_bytes = spec.size() * sizeof(double);
+    // smallest cluster whose bands fit shared memory (a cluster barrier costs ~6x a
+    // CTA barrier): rhs in shared memory if it fits too, else read through L1
+    for (int C = 1; C <= 16; C *= 2)
+        for (int bsm = 1; bsm >= 0; --bsm) {
+            int R = (op.ncy + C - 1) / C;
+            R = (R + 31) / 32 * 32;  // whole 32-row blocks
+            if (R > 32 * kMaxRowBlocks) continue;
+            if ((op.ncy + R - 1) / R < C) continue;  // no empty CTAs
+            const size_t bytes = (size_t(R + 2) * T.pitch + (bsm ? size_t(R) * T.bpitch : 0)) * sizeof(double) +
+                                 spec_bytes;
+            if (bytes <= cap) {
+                T.csize = (op.ncy + R - 1) / R;
+                T.band = R;
+                T.bsmem = bsm;
+                smem = bytes;
+                return true;
+            }
+        }
+    return false;
+}
+
+size_t cl_backup_doubles(const ClGeom& T) { return size_t(T.csize) * size_t(T.band + 2) * T.pitch; }
+
+void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
+                      cudaStream_t st) {
+    if (T.bsmem) {
+        if (T.kind == 1) launch_one<1, true>(P, T, spec, backup, smem, st);
+        else if (T.kind == 2) launch_one<2, true>(P, T, spec, backup, smem, st);
+        else launch_one<0, true>(P, T, spec, backup, smem, st);
+    } else {
+        if (T.kind == 1) launch_one<1, false>(P, T, spec, backup, smem, st);
+        else if (T.kind == 2) launch_one<2, false>(P, T, spec, backup, smem, st);
+        else launch_one<0, false>(P, T, spec, backup, smem, st);
+    }
+}
+void set_coarse_cl_smem(size_t bytes) {
+    set_attrs<0, true>(bytes), set_attrs<1, true>(bytes), set_attrs<2, true>(bytes);
+    set_attrs<0, false>(bytes), set_attrs<1, false>(bytes), set_attrs<2, false>(bytes);
+}
+
+}  // namespace fz
+}  // namespace ismgb

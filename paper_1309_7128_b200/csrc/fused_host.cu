@@ -22,8 +22,9 @@ struct FusedEngine {
     cudaGraphExec_t graph = nullptr;
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
-    int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs
+    int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands
     TmGeom tm{};
+    ClGeom cl{};
     double* tm_spec = nullptr;
     int graph_slots = 0;
     size_t smem = 0;
@@ -56,7 +57,9 @@ static void capture_graph(FusedEngine& e, int slots) {
     cudaGraph_t g;
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
-        if (e.coarse_kind == 2)
+        if (e.coarse_kind == 3)
+            launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
+        else if (e.coarse_kind == 2)
             launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
         else if (e.coarse_kind == 1)
             launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
@@ -126,10 +129,17 @@ FusedEngine* make_fused(Solver& s) {
     // coarse-visit kernel: TMEM-resident rhs when the operator allows it,
     // else shared-memory iterate, else the global-memory wavefront
     std::vector<double> spec;
-    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "tmem" | "smem" | "global"
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "cl" | "tmem" | "smem" | "global"
+    const bool allow_cl = !force || std::string(force) == "cl";
     const bool allow_tmem = !force || std::string(force) == "tmem";
-    const bool allow_smem = !force || std::string(force) != "global";
-    if (allow_tmem && tmem_coarse_plan(L.h, e->tm, spec, e->coarse_smem)) {
+    const bool allow_smem = !force || std::string(force) == "smem" || std::string(force) == "tmem";
+    if (allow_cl && cl_coarse_plan(L.h, e->cl, spec, e->coarse_smem)) {
+        e->coarse_kind = 3;
+        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
+        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * cl_backup_doubles(e->cl)));
+        set_coarse_cl_smem(e->coarse_smem);
+    } else if (allow_tmem && tmem_coarse_plan(L.h, e->tm, spec, e->coarse_smem)) {
         e->coarse_kind = 2;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
         ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
@@ -266,6 +276,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.coarse_visits = st.coarse_launches;
     s.last.coarse_ms = double(st.coarse_ns) * 1e-6;
     s.last.coarse_steps = st.coarse_steps;
+    s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
     s.last.kernel_launches = 2 * launched_slots + 2;
 }
 

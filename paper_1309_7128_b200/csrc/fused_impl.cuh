@@ -34,6 +34,7 @@ struct Ctl {
     long long total, fine, coarse, restrictions, prolongations;
     long long passes, coarse_launches;
     long long coarse_ns, coarse_steps;  // device-timed coarse visits (globaltimer) and their wavefront steps
+    long long coarse_group_ns;          // ... of which inside the wavefront groups
     double r, prev, shift, rc;
     double* buf[2];
     const double* b;
@@ -265,6 +266,22 @@ struct TmGeom {
     bool five;
     double stdw[9];
 };
+// Cluster coarse visit (coarse_cl.cu): row bands over the CTAs of one cluster.
+struct ClGeom {
+    int ncx, ncy;
+    int pitch, bpitch;  // shared-memory row pitches (3 mod 16 doubles)
+    int csize, band;    // cluster size (CTAs), rows per CTA band
+    int bsmem;          // rhs band in shared memory (else read through L1)
+    int ring, ncls, fastdiv, kind;
+    bool five;
+    double stdw[9];
+};
+bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem);
+size_t cl_backup_doubles(const ClGeom& T);
+void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
+                      cudaStream_t st);
+void set_coarse_cl_smem(size_t bytes);
+
 bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem);
 void launch_coarse_tmem(const Params& P, const TmGeom& T, const double* spec, double* backup, size_t smem,
                         cudaStream_t st);
