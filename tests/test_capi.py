@@ -61,3 +61,55 @@ def test_large_operator_matches_port(port):
         a = build_ismg_operator(g)
         b = port.build_ismg_operator(g)
         assert a[0] == b[0] and np.array_equal(a[2], b[2])
+
+
+def _gxx(args, tmp_path):
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ absent")
+    r = subprocess.run(["g++", "-std=c++20", "-O0", "-fsyntax-only"] + args, capture_output=True, text=True,
+                       cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_cpp_facade_compiles_with_reference_shaped_types(tmp_path):
+    """include/ismg_b200.hpp is duck-typed over the reference's value types."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "facade.cpp"
+    src.write_text(r'''
+#include <array>
+#include <cstdint>
+#include <vector>
+#include "ismg_b200.hpp"
+enum class BcKind { dirichlet_velocity, symmetry_fixed_pressure, periodic, inlet };
+enum class Scheme { plain_gs, ismg, gmg, acm };
+struct BoundaryCondition { BcKind kind{}; double u_wall = 0, v_wall = 0, p_wall = 0, v_inflow = 0;
+                           int inlet_start = 0, inlet_width = 0; };
+struct GridSpec { int nx = 8, ny = 8; double h = 1; int tile = 4; std::array<BoundaryCondition, 4> bc{}; };
+struct CycleConfig { Scheme scheme = Scheme::ismg; int tile = 4, depth = 4; double tol_fine = 1e-6, tol_coarse = 1e-5;
+                     long max_total_sweeps = 20000; int acm_pre_smooth = 0, acm_post_smooth = 1; double stall_factor = 0.9; };
+struct ScalarField { int nx = 8, ny = 8; std::vector<double> data = std::vector<double>(100); };
+struct StepMetrics { std::int64_t fine_sweeps = 0, coarse_sweeps = 0, sync_fine = 0, sync_coarse = 0;
+                     double lap_equiv = 0; std::int64_t restrictions = 0, prolongations = 0; };
+struct RunMetrics { std::int64_t fine_cells = 64; StepMetrics current; };
+void use(ismg_b200::Context& ctx) {
+    GridSpec g; CycleConfig c; ScalarField x, b; RunMetrics m;
+    ismg_b200::PressureSolver s(g, c, ctx);
+    ismg_b200::ConvergenceReport r = s.solve(x, b, m);
+    (void)r;
+}
+''')
+    _gxx(["-I", os.path.join(root, "include"), str(src)], tmp_path)
+
+
+def test_cpp_dropin_example_compiles_against_reference(tmp_path):
+    """examples/dropin_solve.cpp: the reference's own types driving the facade."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers absent")
+    _gxx(["-I", os.path.join(root, "include"), "-I", ref, os.path.join(root, "examples", "dropin_solve.cpp")],
+         tmp_path)
