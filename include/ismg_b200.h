@@ -164,9 +164,16 @@ int ismg_device_count(int* out);
 int ismg_ctx_create(int device, void* stream, ismg_ctx** out);
 int ismg_ctx_destroy(ismg_ctx* ctx);
 int ismg_ctx_synchronize(ismg_ctx* ctx);
-/* multi-GPU (strip decomposition along y): attach an NCCL
- * communicator identified by a 128-byte ncclUniqueId shared by all ranks. */
+/* multi-GPU (strip decomposition along y; no reference
+ * counterpart — the reference is single-core). Rank 0 makes a 128-byte
+ * ncclUniqueId, the caller shares it, every rank attaches it to its context
+ * BEFORE creating solvers; fused solves on that context then own the rank's
+ * strip of fine rows, exchange halo rows / scalars / coarse rhs over NCCL and
+ * return the full solution on every rank. */
+int ismg_nccl_unique_id(void* out, size_t bytes);
 int ismg_ctx_attach_comm(ismg_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+/* rows [r0, r1) of a rank: whole coarse tiles, as even as possible (host only) */
+int ismg_strip_rows(int ny, int tile, int nranks, int rank, int32_t* r0, int32_t* r1);
 
 /* ---- host-side geometry (no device needed) -------------------------------- */
 /* GridSpec::validate — grid.hpp:79-96 */

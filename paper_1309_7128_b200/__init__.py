@@ -6,5 +6,5 @@ sm_100a library libismg_b200.so through its C-ABI (`solver`).
 from .api import *  # noqa: F401,F403
 from .solver import (  # noqa: F401
     CaseResult, Context, DeviceField, DeviceState, DeviceVelocity, PressureSolver, apply_scalar_bc,
-    apply_velocity_bc, build_gmg_operator, build_ismg_operator, correct, device_count, divergence, predictor,
-    run_case, step)
+    apply_velocity_bc, build_gmg_operator, build_ismg_operator, correct, device_count, divergence, nccl_unique_id,
+    predictor, run_case, step, strip_rows)

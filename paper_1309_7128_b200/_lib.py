@@ -50,6 +50,8 @@ SIGNATURES = {
     "ismg_ctx_destroy": [VP],
     "ismg_ctx_synchronize": [VP],
     "ismg_ctx_attach_comm": [VP, VP, C.c_int, C.c_int],
+    "ismg_nccl_unique_id": [VP, C.c_size_t],
+    "ismg_strip_rows": [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
     "ismg_grid_validate": [G],
     "ismg_cycle_validate": [CF],
     "ismg_pressure_bc": [G, I32P, I32P],

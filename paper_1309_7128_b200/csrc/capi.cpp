@@ -529,12 +529,31 @@ int ismg_step(ismg_state* st, ismg_solver* s, ismg_report* rep, ismg_step_metric
     });
 }
 
+int ismg_nccl_unique_id(void* out, size_t bytes) {
+    return guard([&] {
+        need(out, "out");
+        if (bytes < 128) fail(ISMG_ERR_INVALID_ARGUMENT, "unique id buffer must hold 128 bytes");
+        nccl_unique_id(out);
+    });
+}
+
 int ismg_ctx_attach_comm(ismg_ctx* c, const void* id, int rank, int nranks) {
     return guard([&] {
         need(c, "ctx");
         need(id, "unique id");
-        if (nranks != 1 || rank != 0)
-            fail(ISMG_ERR_NCCL, "multi-GPU communicator not built into this library version");
+        Ctx& x = c->impl;
+        if (x.comm) fail(ISMG_ERR_INVALID_ARGUMENT, "context already has a communicator");
+        x.comm = make_comm(x.device, id, rank, nranks);
+    });
+}
+
+int ismg_strip_rows(int ny, int tile, int nranks, int rank, int32_t* r0, int32_t* r1) {
+    return guard([&] {
+        need(r0, "r0");
+        need(r1, "r1");
+        int a = 0, b = 0;
+        strip_rows(ny, tile, nranks, rank, &a, &b);
+        *r0 = a, *r1 = b;
     });
 }
 

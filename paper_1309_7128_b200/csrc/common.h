@@ -90,6 +90,17 @@ struct TileAxisH {
     TileAxisH(int n, int tile, bool periodic);
 };
 
+// Strip decomposition (multi-GPU): rows [r0, r1) of `rank` are whole tiles, as
+// even as possible (the first ntiles % nranks ranks take one more tile).
+__host__ __device__ inline void strip_of(int ny, int tile, int nranks, int rank, int* r0, int* r1) {
+    const int ntiles = (ny + tile - 1) / tile;
+    const int base = ntiles / nranks, extra = ntiles % nranks;
+    const int t0 = rank * base + (rank < extra ? rank : extra);
+    const int t1 = t0 + base + (rank < extra ? 1 : 0);
+    *r0 = t0 * tile < ny ? t0 * tile : ny;
+    *r1 = t1 * tile < ny ? t1 * tile : ny;
+}
+
 struct CoarseOpH {
     int ncx = 0, ncy = 0;
     TileAxisH ax, ay;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "common.h"
@@ -21,8 +22,21 @@ struct Scratch {
     static constexpr int kScalars = 64;
 };
 
-struct Comm;  // multi-GPU (comm.cpp)
+// multi-GPU (comm.cpp): NCCL communicator of the strip decomposition
+struct Comm {
+    void* nccl = nullptr;  // ncclComm_t
+    int rank = 0, nranks = 1;
+    long long collectives = 0;  // NCCL calls issued (stats)
+};
+Comm* make_comm(int device, const void* unique_id, int rank, int nranks);
 void destroy_comm(Comm* c);
+void nccl_unique_id(void* out128);
+void strip_rows(int ny, int tile, int nranks, int rank, int* r0, int* r1);
+void comm_reduce_scalars(Comm& c, double* v, int nmax, int nsum, cudaStream_t st);
+void comm_gather_rows(Comm& c, double* origin, int64_t pitch, const std::vector<std::pair<int, int>>& rows,
+                      cudaStream_t st);
+void comm_halo(Comm& c, double* const send[2], double* const recv[2], size_t count, cudaStream_t st);
+void comm_allgather(Comm& c, const double* pack, double* gathered, size_t count, cudaStream_t st);
 
 struct Ctx {
     int device = 0;

@@ -319,14 +319,14 @@ __global__ void __launch_bounds__(kThreads) fine_pass_kernel(Params P) {
     else if (st.phase == kResid) prolong_body(sm, P, st, false);
 }
 
-// final anchor + copy into the caller's field: x = buf[cur] + c
+// final anchor + copy into the caller's field: x = buf[cur] + c (the rank's rows)
 __global__ void finalize_kernel(Params P, View xuser) {
     const Ctl* s = P.ctl;
     const double* src = s->buf[s->cur];
     const bool sh = s->has_shift != 0;
     const double c = s->shift;
     if (s->cur == 0 && !sh) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = P.row0 + int(blockIdx.y);
     if (i >= P.nx) return;
     const double v = src[int64_t(j) * P.pitch + i];
     xuser.at(i, j) = sh ? v + c : v;
@@ -336,8 +336,41 @@ void launch_fine_pass(const Params& P, dim3 grid, size_t, cudaStream_t st) { fin
 size_t fine_pass_smem() { return 0; }  // static shared memory (sizeof(Smem) < 48 KB)
 void set_fine_pass_smem(size_t) {}
 void launch_finalize(const Params& P, View xuser, cudaStream_t st) {
-    finalize_kernel<<<dim3((P.nx + 255) / 256, P.ny), 256, 0, st>>>(P, xuser);
+    finalize_kernel<<<dim3((P.nx + 255) / 256, P.row1 - P.row0), 256, 0, st>>>(P, xuser);
 }
+
+// multi-GPU, after the allgather of every rank's pack: reduce the pass partials
+// in rank order (max|r|, max|tile sum| by MAX; sum x by a fixed-order SUM, so
+// every rank decides on identical values), assemble the coarse rhs from the
+// ranks' coarse rows, and apply the reference's branch logic. The next pass
+// reads its halo rows straight from the gathered packs.
+__global__ void mp_unpack_kernel(Params P) {
+    const double* g = P.gathered;
+    const int L = P.pack_len;
+    // coarse rhs rows of every rank -> cb (used by the next coarse visit)
+    for (int r = 0; r < P.nranks; ++r) {
+        int f0, f1;
+        strip_of(P.ny, P.tile, P.nranks, r, &f0, &f1);
+        const int c0 = f0 / P.tile, c1 = (f1 + P.tile - 1) / P.tile;
+        const double* src = g + int64_t(r) * L + 8;
+        for (int k = threadIdx.x; k < (c1 - c0) * P.ncx; k += blockDim.x) {
+            const int jj = k / P.ncx, I = k - jj * P.ncx;
+            P.cb.at(I, c0 + jj) = src[int64_t(jj) * P.cb.pitch + I];
+        }
+    }
+    if (threadIdx.x == 0 && g[2] != 0.0) {  // a fine pass ran in this slot (all ranks alike)
+        double m = 0.0, c = 0.0, sx = 0.0;
+        for (int r = 0; r < P.nranks; ++r) {
+            const double* v = g + int64_t(r) * L;
+            m = fmax(m, v[0]);
+            c = fmax(c, v[1]);
+            sx += v[4];
+        }
+        fine_decide(P, int(g[3]), m, sx, c);
+    }
+    if (threadIdx.x == 0) P.rank_part[2] = 0.0;  // this rank's pass flag, for the next slot
+}
+void launch_mp_unpack(const Params& P, cudaStream_t st) { mp_unpack_kernel<<<1, 1024, 0, st>>>(P); }
 
 }  // namespace fz
 }  // namespace ismgb

@@ -104,7 +104,42 @@ struct Geo {
     double c, fwS, fwN;
     double* outp;
     int64_t pitch;
+    // multi-GPU: rows [hj0, hj0+3) also go to hs0, rows [hj1, hj1+3) to hs1 (nullptr: none)
+    double* hs0;
+    double* hs1;
+    int hj0, hj1;
 };
+
+__device__ __forceinline__ void halo_geo(Geo& G, const Params& P, int c0) {
+    G.hs0 = G.hs1 = nullptr;
+    G.hj0 = G.hj1 = -1000;
+    if (!P.mp) return;
+    if (P.row0 > 0) G.hs0 = P.halo_send[0] + kXOff + c0, G.hj0 = P.row0;
+    if (P.row1 < P.ny) G.hs1 = P.halo_send[1] + kXOff + c0, G.hj1 = P.row1 - 3;
+}
+
+// store a finished quad row j (and its halo copy for the neighbour rank)
+__device__ __forceinline__ void put_row(const Geo& G, const Lane& L, int j, const double* v) {
+    double* dst = G.outp + int64_t(j) * G.pitch;
+    double* hs = nullptr;
+    if (unsigned(j - G.hj0) < 3u) hs = G.hs0 + int64_t(j - G.hj0) * G.pitch;
+    if (unsigned(j - G.hj1) < 3u) hs = G.hs1 + int64_t(j - G.hj1) * G.pitch;
+    if (!L.spec) {
+        reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
+        if (hs) {
+            reinterpret_cast<double2*>(hs)[0] = make_double2(v[0], v[1]);
+            reinterpret_cast<double2*>(hs)[1] = make_double2(v[2], v[3]);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (L.dom[q]) {
+                dst[q] = v[q];
+                if (hs) hs[q] = v[q];
+            }
+    }
+}
 
 __device__ __forceinline__ double row_part(const Geo& G, int j) {
     return ((j > 0) ? 1.0 : G.fwS) + ((j < G.ny - 1) ? 1.0 : G.fwN);  // smoother.hpp:60-61
@@ -138,10 +173,6 @@ __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L,
             for (int q = 0; q < 4; ++q) t[q] = L.dom[q] ? t[q] : 0.0;
         }
         w.b[s0][0] = b01.x, w.b[s0][1] = b01.y, w.b[s0][2] = b23.x, w.b[s0][3] = b23.y;
-#ifdef ISMG_DBG
-        if (blockIdx.x == 0 && blockIdx.y == 1 && (L.l == 5 || L.l == 25) && k <= G.r0 + 3)
-            printf("load k=%d U=%d slot=%d lane=%d raw=%g t=%g\n", k, U, slot, L.l, v01.x, t[0]);
-#endif
     }
     double* x1 = w.x[s1];
     double* x2 = w.x[s2];
@@ -212,19 +243,7 @@ __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L,
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));  // std::max(rmax, |r|): NaN dropped
             A.sx = A.sx + ((x3[0] + x3[1]) + (x3[2] + x3[3]));   // out-of-domain cells hold 0
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            double* dst = G.outp + int64_t(j) * G.pitch;
-#ifdef ISMG_DBG
-            if (blockIdx.x == 0 && blockIdx.y == 1 && (L.l == 5 || L.l == 25) && j <= G.r0 + 1)
-                printf("res k=%d j=%d lane=%d x3=%g x4=%g x2=%g b=%g dst=%p\n", k, j, L.l, x3[0], x4[0], x2[0], b[0], dst);
-#endif
-            if (!L.spec) {
-                reinterpret_cast<double2*>(dst)[0] = make_double2(x3[0], x3[1]);
-                reinterpret_cast<double2*>(dst)[1] = make_double2(x3[2], x3[3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (L.dom[q]) dst[q] = x3[q];
-            }
+            put_row(G, L, j, x3);
         }
     }
     // row k takes the slot of row k-4
@@ -239,7 +258,7 @@ __device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int
     double v = A.tacc;
     for (int o = g >> 1; o > 0; o >>= 1) v = v + __shfl_down_sync(kFull, v, o);
     if (L.owned && ((L.l - 1) & (g - 1)) == 0 && L.dom[0]) {
-        P.cb.at(L.c0 >> lg, j >> lg) = v;
+        P.cbw.at(L.c0 >> lg, j >> lg) = v;
         A.cm = max_drop_nan(A.cm, fabs(v));
         A.nan |= (v != v);  // a NaN residual poisons its tile sum
     }
@@ -277,7 +296,12 @@ __device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double 
     s = warp_sum_down(s);
     c = warp_max(c);
     if ((threadIdx.x & 31) == 0) {
-        fine_decide(P, mode, m, s, c);
+        if (P.mp) {  // all-reduced across ranks, then mp_decide_kernel
+            P.rank_part[0] = m, P.rank_part[1] = c, P.rank_part[2] = 1.0, P.rank_part[3] = double(mode);
+            P.rank_part[4] = s;
+        } else {
+            fine_decide(P, mode, m, s, c);
+        }
         *P.ticket = 0u;
         __threadfence();
     }
@@ -290,14 +314,15 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     const int a = blockIdx.x * W;
     const Lane L(P, a, nq);
     Geo G;
-    G.r0 = blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.ny), G.ny = P.ny;
+    G.r0 = P.row0 + blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.row1), G.ny = P.ny;
     G.c = st.has_shift ? st.shift : -0.0;  // x + (-0.0) == x for every x
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
+    halo_geo(G, P, L.c0);
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
-    const double* xrow0 = st.buf[st.cur] + (a - 4);
+    const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
     const int kfirst = G.r0 - 3, klast = G.r1 + 2;
     if ((threadIdx.x & 31) == 0) {
@@ -306,7 +331,7 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     }
     __syncwarp();
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
-        issue_row_w(sm, xrow0 + int64_t(kfirst + s) * G.pitch, brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+        issue_row_w(sm, row_src(P, xin, kfirst + s, a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     Win w;
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -324,8 +349,7 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
         if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
         __syncwarp();  // every lane has read the slot of row k
         if (k + kRingW <= klast)
-            issue_row_w(sm, xrow0 + int64_t(k + kRingW) * G.pitch, brow0 + int64_t(k + kRingW) * G.pitch, slot,
-                        bytes);
+            issue_row_w(sm, row_src(P, xin, k + kRingW, a - 4), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     };
     // kfirst = r0 - 3 = 1 (mod 4) (P.H is a multiple of 4), so in the block
@@ -347,14 +371,15 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     const int a = blockIdx.x * W;
     const Lane L(P, a, nq);
     Geo G;
-    G.r0 = blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.ny), G.ny = P.ny;
+    G.r0 = P.row0 + blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.row1), G.ny = P.ny;
     G.c = st.has_shift ? st.shift : -0.0;
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
+    halo_geo(G, P, L.c0);
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
-    const double* xrow0 = st.buf[st.cur] + (a - 4);
+    const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
     Acc A;
     // TileAxis::locate_cell of the lane's columns
@@ -375,7 +400,7 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     }
     __syncwarp();
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
-        issue_row_w(sm, xrow0 + int64_t(kfirst + s) * G.pitch, brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+        issue_row_w(sm, row_src(P, xin, kfirst + s, a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     const uint32_t bar0 = su32(&sm.bar[0]);
     double x1[4] = {0, 0, 0, 0}, x2[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
     int slot = 0;
@@ -425,25 +450,14 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
             A.sx = A.sx + ((x1[0] + x1[1]) + (x1[2] + x1[3]));
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            if (prolong) {
-                double* dst = G.outp + int64_t(j) * G.pitch;
-                if (!L.spec) {
-                    reinterpret_cast<double2*>(dst)[0] = make_double2(x1[0], x1[1]);
-                    reinterpret_cast<double2*>(dst)[1] = make_double2(x1[2], x1[3]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (L.dom[q]) dst[q] = x1[q];
-                }
-            }
+            if (prolong) put_row(G, L, j, x1);
         }
         if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
 #pragma unroll
         for (int q = 0; q < 4; ++q) x2[q] = x1[q], x1[q] = x0[q], b1[q] = b0[q];
         __syncwarp();
         if (k + kRingW <= klast)
-            issue_row_w(sm, xrow0 + int64_t(k + kRingW) * G.pitch, brow0 + int64_t(k + kRingW) * G.pitch, slot,
-                        bytes);
+            issue_row_w(sm, row_src(P, xin, k + kRingW, a - 4), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     }
     warp_epilogue(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan);

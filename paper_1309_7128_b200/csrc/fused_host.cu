@@ -19,18 +19,21 @@ struct FusedEngine {
     DevBuf scratch;        // second ping-pong buffer
     int* d_log = nullptr;
     std::vector<int> h_log;
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // 8, 16, 32, 64 slots, captured once
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
     int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands
     TmGeom tm{};
     ClGeom cl{};
     double* tm_spec = nullptr;
-    int graph_slots = 0;
     size_t smem = 0;
     int fine_kind = 0;  // 0 column pairs (256-column CTA strips), 2 one-warp strips of column quads
     dim3 grid;
     cudaEvent_t ev = nullptr;
+    // multi-GPU strip decomposition (P.mp): this rank's pack and all ranks' packs
+    double* pack = nullptr;
+    double* gathered = nullptr;
+    std::vector<std::pair<int, int>> fine_rows, coarse_rows;  // per rank
 };
 
 bool fused_supported(const Solver& s) {
@@ -50,10 +53,22 @@ static void launch_fine(const FusedEngine& e, cudaStream_t st) {
     else launch_fine_pass(e.P, e.grid, e.smem, st);
 }
 
-static void capture_graph(FusedEngine& e, int slots) {
+// multi-GPU, after every fine-pass slot: all-reduce the pass partials (MAX of
+// max|r|, max|tile sum|, flag, mode; SUM of sum x), gather every rank's coarse
+// rhs rows, apply the branch logic, refresh the halo rows.
+static void mp_exchange(FusedEngine& e, Ctx& c) {
+    comm_allgather(*c.comm, e.pack, e.gathered, size_t(e.P.pack_len), c.stream);
+    launch_mp_unpack(e.P, c.stream);
+}
+
+static int slot_index(int slots) { return slots <= 8 ? 0 : (slots <= 16 ? 1 : (slots <= 32 ? 2 : 3)); }
+
+// The graph of `slots` [coarse-visit, fine-pass (+ exchange)] slots, captured on
+// first use and kept for the engine's lifetime (capturing NCCL calls is costly).
+static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
+    cudaGraphExec_t& ge = e.graphs[slot_index(slots)];
+    if (ge) return ge;
     Ctx& c = *e.s->ctx;
-    if (e.graph) cudaGraphExecDestroy(e.graph);
-    e.graph = nullptr;
     cudaGraph_t g;
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
@@ -66,11 +81,12 @@ static void capture_graph(FusedEngine& e, int slots) {
         else
             launch_coarse_global(e.P, c.stream);
         launch_fine(e, c.stream);
+        if (e.P.mp) mp_exchange(e, c);
     }
     ISMG_CUDA(cudaStreamEndCapture(c.stream, &g));
-    ISMG_CUDA(cudaGraphInstantiate(&e.graph, g, 0));
+    ISMG_CUDA(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    e.graph_slots = slots;
+    return ge;
 }
 
 FusedEngine* make_fused(Solver& s) {
@@ -94,8 +110,44 @@ FusedEngine* make_fused(Solver& s) {
         const int v = atoi(h);
         if (v > 0) P.H = std::max(P.tile, v / P.tile * P.tile);
     }
+    // strip decomposition over the context's NCCL ranks (one-warp kernel only)
+    P.row0 = 0, P.row1 = P.ny, P.mp = 0;
+    if (c.comm && c.comm->nranks > 1 && e->fine_kind == 2) {
+        const int R = c.comm->nranks;
+        for (int r = 0; r < R; ++r) {
+            int a = 0, b = 0;
+            strip_rows(P.ny, P.tile, R, r, &a, &b);
+            e->fine_rows.emplace_back(a, b);
+            e->coarse_rows.emplace_back(a / P.tile, (b + P.tile - 1) / P.tile);
+        }
+        P.row0 = e->fine_rows[size_t(c.comm->rank)].first, P.row1 = e->fine_rows[size_t(c.comm->rank)].second;
+        P.mp = 1;
+        P.nranks = R;
+        // pack = [8 scalars | this rank's coarse rows (pitched) | 3 first rows | 3 last rows]
+        const int rank = c.comm->rank;
+        const int64_t cpitch = L.b->view().pitch;
+        int maxc = 0;
+        for (auto& cr : e->coarse_rows) maxc = std::max(maxc, cr.second - cr.first);
+        P.pack_cb_rows = maxc;
+        const int64_t cbr = int64_t(maxc) * cpitch;
+        int64_t len = 8 + cbr + 6 * P.pitch;
+        len = (len + 15) / 16 * 16;
+        P.pack_len = int(len);
+        ISMG_CUDA(cudaMalloc(&e->pack, sizeof(double) * size_t(len)));
+        ISMG_CUDA(cudaMemset(e->pack, 0, sizeof(double) * size_t(len)));
+        ISMG_CUDA(cudaMalloc(&e->gathered, sizeof(double) * size_t(len) * size_t(R)));
+        ISMG_CUDA(cudaMemset(e->gathered, 0, sizeof(double) * size_t(len) * size_t(R)));
+        P.rank_part = e->pack;
+        P.gathered = e->gathered;
+        const int cr0 = e->coarse_rows[size_t(rank)].first;
+        P.cbw = View{e->pack + 8 - int64_t(cr0) * cpitch, cpitch, L.h.ncx, L.h.ncy};
+        P.halo_send[0] = e->pack + 8 + cbr;
+        P.halo_send[1] = e->pack + 8 + cbr + 3 * P.pitch;
+        P.halo_recv[0] = rank > 0 ? e->gathered + int64_t(rank - 1) * len + 8 + cbr + 3 * P.pitch : nullptr;
+        P.halo_recv[1] = rank + 1 < R ? e->gathered + int64_t(rank + 1) * len + 8 + cbr : nullptr;
+    }
     P.nstrips = (P.nx + width - 1) / width;
-    P.nchunks = (P.ny + P.H - 1) / P.H;
+    P.nchunks = std::max(1, (P.row1 - P.row0 + P.H - 1) / P.H);
     P.bc = s.bc;
     P.singular = s.singular ? 1 : 0;
     P.nslots = L.h.stencil_points();
@@ -104,6 +156,7 @@ FusedEngine* make_fused(Solver& s) {
     P.ncells = double(int64_t(P.nx) * P.ny);
     P.cb = L.b->view();
     P.ce = L.x->view();
+    if (!P.mp) P.cbw = P.cb;
     P.w = L.d_w;
     P.ax = L.ax, P.ay = L.ay;
     const int nb = P.nstrips * P.nchunks;
@@ -157,13 +210,16 @@ FusedEngine* make_fused(Solver& s) {
 
 void destroy_fused(FusedEngine* e) {
     if (!e) return;
-    if (e->graph) cudaGraphExecDestroy(e->graph);
+    for (auto& ge : e->graphs)
+        if (ge) cudaGraphExecDestroy(ge);
     e->scratch.free();
     cudaFree(e->P.part);
     cudaFree(e->P.ticket);
     cudaFree(e->d_log);
     cudaFree(e->coarse_backup);
     cudaFree(e->tm_spec);
+    cudaFree(e->pack);
+    cudaFree(e->gathered);
     cudaFree(e->d_ctl);
     cudaFreeHost(e->h_ctl);
     if (e->ev) cudaEventDestroy(e->ev);
@@ -179,6 +235,7 @@ double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters) {
     Ctx& c = *s.ctx;
     if (x.buf.pitch != e.P.pitch || b.buf.pitch != e.P.pitch)
         fail(ISMG_ERR_INTERNAL, "fused path: field pitch mismatch");
+    if (e.P.mp) fail(ISMG_ERR_INVALID_ARGUMENT, "bench_fine_pass: single-GPU contexts only");
     k_zero_ghosts(c, x.view());
     Ctl init{};
     init.phase = kFine;
@@ -227,14 +284,27 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     init.b = b.buf.origin();
     *e.h_ctl = init;
     ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    if (e.P.mp) {  // first halo rows: this rank's boundary rows of x to the neighbours
+        const size_t rows3 = size_t(3) * size_t(e.P.pitch);
+        const double* row0 = x.buf.origin() - kXOff;  // start of logical row 0
+        ISMG_CUDA(cudaMemsetAsync(e.pack, 0, 8 * sizeof(double), c.stream));  // no pass yet
+        if (e.P.row0 > 0)
+            ISMG_CUDA(cudaMemcpyAsync(e.P.halo_send[0], row0 + int64_t(e.P.row0) * e.P.pitch, rows3 * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, c.stream));
+        if (e.P.row1 < e.P.ny)
+            ISMG_CUDA(cudaMemcpyAsync(e.P.halo_send[1], row0 + int64_t(e.P.row1 - 3) * e.P.pitch,
+                                      rows3 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        comm_allgather(*c.comm, e.pack, e.gathered, size_t(e.P.pack_len), c.stream);
+        c.comm->collectives += 1;
+    }
     // launch batches of [coarse-visit, fine-pass] slots until the phase is done
     int slots = 8;
     long long launched_slots = 0;
     int since_poll = 0;
     for (;;) {
-        if (!e.graph || e.graph_slots != slots) capture_graph(e, slots);
-        ISMG_CUDA(cudaGraphLaunch(e.graph, c.stream));
-        c.launches += 2 * slots;
+        ISMG_CUDA(cudaGraphLaunch(graph_for(e, slots), c.stream));
+        c.launches += (e.P.mp ? 3 : 2) * slots;
+        if (c.comm && e.P.mp) c.comm->collectives += slots;
         launched_slots += slots;
         ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
         ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
@@ -248,6 +318,10 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     (void)since_poll;
     launch_finalize(e.P, x.view(), c.stream);
     c.launches += 1;
+    if (e.P.mp) {  // every rank's strip of the solution to every rank
+        comm_gather_rows(*c.comm, x.buf.origin() - kXOff, e.P.pitch, e.fine_rows, c.stream);
+        c.comm->collectives += c.comm->nranks;
+    }
     ISMG_CUDA(cudaGetLastError());
     const Ctl& st = *e.h_ctl;
     // replay the sweep sequence into the metrics (lap_equiv order, metrics.hpp:46-56)
@@ -276,8 +350,9 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.coarse_visits = st.coarse_launches;
     s.last.coarse_ms = double(st.coarse_ns) * 1e-6;
     s.last.coarse_steps = st.coarse_steps;
+    s.last.collectives = c.comm ? c.comm->collectives : 0;
     s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
-    s.last.kernel_launches = 2 * launched_slots + 2;
+    s.last.kernel_launches = (e.P.mp ? 3 : 2) * launched_slots + 2;
 }
 
 }  // namespace ismgb

@@ -58,7 +58,31 @@ struct Params {
     int* visit_log;  // (coarse sweeps, fine sweeps) per coarse visit
     int visit_cap;
     double* coarse_scratch;  // reduction scratch for the coarse kernel
+    // strip decomposition (multi-GPU): this rank relaxes fine rows [row0, row1);
+    // rows row0-3..row0-1 / row1..row1+2 come from the neighbours through
+    // halo_recv, its own first / last 3 rows go out through halo_send (3 pitched
+    // rows each, column origin kXOff). With mp set the last CTA stores the
+    // rank's partials in rank_part [max|r|, max|tile sum|, pass flag, mode, sum x]
+    // and mp_decide_kernel applies the branch logic to the all-reduced values.
+    int row0, row1, mp;
+    double* halo_send[2];
+    const double* halo_recv[2];
+    double* rank_part;
+    View cbw;  // where the fused pass writes its tile sums (cb; multi-GPU: the rank's pack)
+    // multi-GPU pack: per rank `pack_len` doubles = [8 scalars | coarse rows | 2 x 3 halo rows]
+    const double* gathered;  // all ranks' packs after the allgather
+    int nranks, pack_len, pack_cb_rows;
 };
+
+// x-row source of the fused passes: the rank's own rows from the field, the
+// neighbours' rows from the halo buffers (multi-GPU only)
+__device__ __forceinline__ const double* row_src(const Params& P, const double* xin, int k, int col) {
+    if (P.mp) {
+        if (k < P.row0 && P.row0 > 0) return P.halo_recv[0] + int64_t(k - (P.row0 - 3)) * P.pitch + kXOff + col;
+        if (k >= P.row1 && P.row1 < P.ny) return P.halo_recv[1] + int64_t(k - P.row1) * P.pitch + kXOff + col;
+    }
+    return xin + int64_t(k) * P.pitch + col;
+}
 
 __device__ __forceinline__ long long gtimer() {
     long long t;
@@ -250,6 +274,7 @@ void set_fine_pass_w_smem();
 dim3 fine_pass_w_grid(const Params& P);
 void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st);
 void launch_finalize(const Params& P, View xuser, cudaStream_t st);
+void launch_mp_unpack(const Params& P, cudaStream_t st);
 void launch_coarse_global(const Params& P, cudaStream_t st);
 void launch_coarse_smem(const Params& P, double* backup, size_t smem, cudaStream_t st);
 void set_coarse_smem(size_t bytes);

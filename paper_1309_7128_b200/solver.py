@@ -47,12 +47,33 @@ class Context:
         _lib.call("ismg_ctx_launch_count", self.h, C.byref(n))
         return n.value
 
+    def attach_comm(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        """Join the NCCL strip decomposition (before creating solvers on this context)."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _lib.call("ismg_ctx_attach_comm", self.h, buf, int(rank), int(nranks))
+
     def __del__(self):
         try:
             if getattr(self, "h", None) and _lib._lib is not None:
                 _lib.lib().ismg_ctx_destroy(self.h)
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 makes it; the caller shares it)."""
+    buf = C.create_string_buffer(128)
+    _lib.call("ismg_nccl_unique_id", buf, 128)
+    return buf.raw
+
+
+def strip_rows(ny: int, tile: int, nranks: int, rank: int) -> tuple:
+    """Fine rows [r0, r1) owned by `rank` in the strip decomposition (whole tiles)."""
+    a, b = C.c_int32(), C.c_int32()
+    _lib.call("ismg_strip_rows", int(ny), int(tile), int(nranks), int(rank), C.byref(a), C.byref(b))
+    return a.value, b.value
 
 
 def device_count() -> int:
