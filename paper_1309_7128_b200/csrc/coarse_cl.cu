@@ -43,13 +43,19 @@ namespace {
 constexpr int kLag = 8;            // wavefront steps between consecutive sweeps
 constexpr int kMaxGroup = 512;     // sweeps per checkpointed group
 constexpr int kPredCap = 32;       // cap of the predicted first group of a visit
-constexpr int kClThreads = 512;
+constexpr int kIntWarps = 16;                  // warps relaxing interior cells
+constexpr int kRingWarps = 8;                  // warps relaxing ring cells: (row block, phase)
+constexpr int kClThreads = 32 * (kIntWarps + kRingWarps);
 
 constexpr int kMaxRowBlocks = 4;  // 32-row blocks per CTA band
 
+// The CTA's dynamic shared memory, addressed by offsets (doubles) so every
+// access compiles to a 32-bit LDS/STS: [iterate band | rhs band | class table].
+extern __shared__ __align__(16) double cl_dyn[];
+
 struct ClShared {
     double cmax[kMaxRowBlocks][kMaxGroup];  // residual max per (row block, sweep of the group)
-    double rmax[kMaxGroup];                 // residual max of the ring cells per sweep
+    unsigned long long rmax[kMaxGroup];     // residual max of the ring cells per sweep (double bits)
     double gmax[kMaxGroup];                 // ... all reduced over the CTA
     double red[32];
     double bcast[4];
@@ -67,8 +73,9 @@ __device__ __forceinline__ int ring_index(const ClGeom& T, int I, int J) {
 struct Nbr {
     double c, e, w, n, s, ne, nw, se, sw;
 };
-// neighbours of the cell at p (row pitch `pitch`; N = row J+1)
-__device__ __forceinline__ Nbr gather(const double* p, int pitch, bool with_c, bool five) {
+// neighbours of the cell at shared offset o (row pitch `pitch`; N = row J+1)
+__device__ __forceinline__ Nbr gather(int o, int pitch, bool with_c, bool five) {
+    const double* p = cl_dyn + o;
     Nbr v;
     v.c = with_c ? p[0] : 0.0;
     v.e = p[1];
@@ -140,10 +147,9 @@ __device__ __forceinline__ double apply_std(const ClGeom& T, const Nbr& v, doubl
 
 // boundary-ring cell: 9 weights + RN(1/w0) of its class (spec table in smem)
 template <bool kResidual>
-__device__ __forceinline__ double ring_cell(const ClGeom& T, const double* spec, const Nbr& v, int I, int J,
-                                         double bIJ) {
-    const int* ring_cls = reinterpret_cast<const int*>(spec + 10 * T.ncls);
-    const double* wc = spec + 10 * ring_cls[ring_index(T, I, J)];
+__device__ __forceinline__ double ring_cell(const ClGeom& T, int so, const Nbr& v, int I, int J, double bIJ) {
+    const int* ring_cls = reinterpret_cast<const int*>(cl_dyn + so + 10 * T.ncls);
+    const double* wc = cl_dyn + so + 10 * ring_cls[ring_index(T, I, J)];
     double w[9];
 #pragma unroll
     for (int sl = 0; sl < 9; ++sl) w[sl] = wc[sl];
@@ -176,14 +182,27 @@ __device__ __forceinline__ double warp_max_nonneg(double m) {
     return __hiloint2double(int(mh), int(ml));
 }
 
+__device__ __forceinline__ void tm_ld2(uint32_t taddr, uint32_t& lo, uint32_t& hi) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(taddr));
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, uint32_t lo, uint32_t hi) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(lo), "r"(hi));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
 struct Band {
     int c, C;       // cluster rank, cluster size
     int J0, J1;     // rows [J0, J1) of this CTA
-    double* xs;     // iterate: row J at xs + (J - J0 + 1) * pitch + 1 (halo rows J0-1, J1)
-    const double* bs;
-    int bpitch;     // rhs: row J at bs + (J - J0) * bpitch (smem) or a global view
+    double* xs;     // iterate: row J at xs + (J - J0 + 1) * pitch + 1 (halo rows J0-1, J1); xs = cl_dyn
+    int bo;         // rhs band (BM == 1): row J at cl_dyn[bo + (J - J0) * bpitch]
+    int bpitch;
+    int so;         // class table offset in cl_dyn
     double* south;  // neighbour CTA's halo row that mirrors row J0 (nullptr at the bottom)
     double* north;  // neighbour CTA's halo row that mirrors row J1 - 1
+    uint32_t tmem;  // TMEM base (BM == 2): lane J - J0, column pair (I + 2J) mod 256 holds b(I, J)
 };
 
 __device__ __forceinline__ void step_sync(const Band& B) {
@@ -193,18 +212,18 @@ __device__ __forceinline__ void step_sync(const Band& B) {
 
 // One group of G sweeps (residuals: also form the residual max of every sweep).
 // One ring cell (boundary row or column) of sweep g at its step: update or residual.
-template <bool BSmem>
-__device__ __forceinline__ double ring_step(const ClGeom& T, const Band& B, const double* spec, const View& cbg,
-                                            int I, int J, bool residual) {
-    double* p = B.xs + (J - B.J0 + 1) * T.pitch + 1 + I;
-    const double bIJ = BSmem ? B.bs[(J - B.J0) * B.bpitch + I] : __ldg(&cbg.p[int64_t(J) * cbg.pitch + I]);
-    const Nbr v = gather(p, T.pitch, residual, T.five);
+template <int BM>
+__device__ __forceinline__ double ring_step(const ClGeom& T, const Band& B, const View& cbg, int I, int J,
+                                            bool residual) {
+    const int o = (J - B.J0 + 1) * T.pitch + 1 + I;
+    const double bIJ = BM == 1 ? cl_dyn[B.bo + (J - B.J0) * B.bpitch + I] : __ldg(&cbg.p[int64_t(J) * cbg.pitch + I]);
+    const Nbr v = gather(o, T.pitch, residual, T.five);
     if (residual) {
-        const double m = fabs(ring_cell<true>(T, spec, v, I, J, bIJ));
+        const double m = fabs(ring_cell<true>(T, B.so, v, I, J, bIJ));
         return (m != m) ? 0.0 : m;  // std::max drops NaN
     }
-    const double out = ring_cell<false>(T, spec, v, I, J, bIJ);
-    *p = out;
+    const double out = ring_cell<false>(T, B.so, v, I, J, bIJ);
+    cl_dyn[o] = out;
     if (J == B.J0 && B.south != nullptr) B.south[I] = out;
     if (J == B.J1 - 1 && B.north != nullptr) B.north[I] = out;
     return 0.0;
@@ -212,128 +231,194 @@ __device__ __forceinline__ double ring_step(const ClGeom& T, const Band& B, cons
 
 // One group of G sweeps (residuals: also form the residual max of every sweep).
 // Interior cells: lane = row J, warps of a row block split the sweeps in
-// flight (g = h mod kH). Ring cells (first / last row and column) go to a
-// separate lane-parallel pass, four lanes per sweep (one per side), so the
-// interior loop never diverges on them.
-template <int Kind, bool BSmem>
-__device__ void cl_group(const ClGeom& T, const Band& B, const double* spec, const View& cbg, ClShared& cs, int G,
-                         bool residuals) {
+// flight (g = h mod kH). Ring cells (first / last row and column) run on
+// their own warps, one per (row block, phase), so the interior warps never
+// diverge on them and the class-table chain stays off their critical path.
+template <int Kind, int BM>
+__device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G, bool residuals) {
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
+    const int nwarps = kIntWarps;
     const int nrb = (B.J1 - B.J0 + 31) >> 5;  // 32-row blocks of the band (1, 2 or 4)
-    const int kH = 1 << (31 - __clz(nwarps / nrb));  // warps per row block (power of two; nrb = 3 idles some)
-    const int rb = warp % nrb, h = warp / nrb;
+    // TMEM rhs: a warp may only read its own lane quadrant, so row block = warp mod 4
+    const int nq = BM == 2 ? 4 : nrb;
+    // warps per row block (power of two; nrb = 3 idles some). Measured (per-warp
+    // clock64 trace, ISMG_CL_TRACE): one cell-pair iteration is a ~500-cycle
+    // dependent chain, so the sweeps in flight are spread over all warps even when
+    // few are in flight (one warp per row block doubled the step time).
+    const int kH = 1 << (31 - __clz(nwarps / nq));
+    const int rb = warp % nq, h = warp / nq;
     const int Jw = B.J0 + 32 * rb;  // first row of the warp
     const int J = Jw + lane;
     const int jlast = min(Jw + 31, B.J1 - 1);
-    const bool rowint = h < kH && J <= jlast && J > 0 && J < T.ncy - 1;  // interior row of the band
+    const bool is_int = warp < kIntWarps;
+    const bool rowint = is_int && rb < nrb && h < kH && J <= jlast && J > 0 && J < T.ncy - 1;  // interior row
     const int pitch = T.pitch;
-    double* rowp = B.xs + (J - B.J0 + 1) * pitch + 1;  // cell (0, J)
-    const double* brow = BSmem ? B.bs + (J - B.J0) * B.bpitch : cbg.p + int64_t(J) * cbg.pitch;
+    // offsets of cell (0, J) of this lane's row (rows outside the band read row J0)
+    const int Jc = (J >= B.J0 && J < B.J1) ? J : B.J0;
+    const int rowo = (Jc - B.J0 + 1) * pitch + 1;
+    const int browo = B.bo + (Jc - B.J0) * B.bpitch;
+    const double* brow = cbg.p + int64_t(Jc) * cbg.pitch;
+    const uint32_t tq = B.tmem + (uint32_t(32 * rb) << 16);  // TMEM lane quadrant of this warp (BM == 2)
     const bool mirror_s = J == B.J0 && B.south != nullptr;
     const bool mirror_n = J == B.J1 - 1 && B.north != nullptr;
     const unsigned nint = unsigned(T.ncx - 2);  // interior columns 1..ncx-2
-    // ring pass: lane 4k+s of warp w handles side s of sweep g = gbase + 8w + k
-    const int rk = lane >> 2, side = lane & 3;
     const bool has_bottom = B.J0 == 0, has_top = B.J1 == T.ncy;
     if (residuals) {
         for (int k = threadIdx.x; k < nrb * kMaxGroup; k += blockDim.x) (&cs.cmax[0][0])[k] = 0.0;
-        for (int k = threadIdx.x; k < kMaxGroup; k += blockDim.x) cs.rmax[k] = 0.0;
+        for (int k = threadIdx.x; k < kMaxGroup; k += blockDim.x) cs.rmax[k] = 0ull;
     }
     __syncthreads();
     const int tau_end = dmax + kLag * (G - 1) + (residuals ? 4 : 0);
     const int dlo = 2 * Jw, dhi = 2 * jlast + T.ncx - 1;
-    const bool int_on = h < kH;
-    const int rw = nwarps - 1 - warp;  // ring passes run on the last warps
+    const bool int_on = is_int && rb < nrb && h < kH;
+    // ring warp: row block rr of the band, one phase (0 update, 1 residual)
+    const int rr = (warp - kIntWarps) >> 1, rph = (warp - kIntWarps) & 1;
+    const bool ring_on = !is_int && rr < nrb && (rph == 0 || residuals);
+    const int Jr = B.J0 + 32 * rr + lane;  // this ring lane's row
+#ifdef ISMG_CL_TRACE
+    long long tr_int = 0, tr_ring = 0, tr_bar = 0;
+#endif
     for (int tau = 0; tau <= tau_end; ++tau) {
+#ifdef ISMG_CL_TRACE
+        const long long c0 = clock64();
+#endif
         // ---- interior cells of this warp's rows: updates on diagonals tau - 8g,
         //      residuals on tau - 4 - 8g; one loop carries one of each, so the two
         //      independent dependency chains overlap
         if (int_on) {
-            const int bu = tau, br = residuals ? tau - 4 : -1;
+            const int bu0 = tau, br0 = residuals ? tau - 4 : -1;
             int gu = 0, guh = -1, gr = 0, grh = -1;
-            if (bu >= dlo) {
-                const int g_lo = max(0, (bu - dhi + kLag - 1) >> 3);
-                guh = min(G - 1, (bu - dlo) >> 3);
+            if (bu0 >= dlo) {
+                const int g_lo = max(0, (bu0 - dhi + kLag - 1) >> 3);
+                guh = min(G - 1, (bu0 - dlo) >> 3);
                 gu = g_lo + ((h - g_lo) & (kH - 1));
             }
-            if (br >= dlo) {
-                const int g_lo = max(0, (br - dhi + kLag - 1) >> 3);
-                grh = min(G - 1, (br - dlo) >> 3);
+            if (br0 >= dlo) {
+                const int g_lo = max(0, (br0 - dhi + kLag - 1) >> 3);
+                grh = min(G - 1, (br0 - dlo) >> 3);
                 gr = g_lo + ((h - g_lo) & (kH - 1));
             }
-            const int Iu0 = bu - 2 * J, Ir0 = br - 2 * J;
+            const int Iu0 = bu0 - 2 * J, Ir0 = br0 - 2 * J;
 #pragma unroll 1
             while (gu <= guh || gr <= grh) {
                 const bool du = gu <= guh, dres = gr <= grh;
                 const int Iu = Iu0 - kLag * gu, Ir = Ir0 - kLag * gr;
                 const bool oku = du && rowint && unsigned(Iu - 1) < nint;
                 const bool okr = dres && rowint && unsigned(Ir - 1) < nint;
-                double m = 0.0;
-                if (okr) {  // residual of sweep gr (inputs final since step tau - 1)
-                    const double bIJ = BSmem ? brow[Ir] : __ldg(brow + Ir);
-                    m = fabs(apply_std<true, Kind>(T, gather(rowp + Ir, pitch, true, T.five), bIJ));
-                    m = (m != m) ? 0.0 : m;  // std::max drops NaN
+                const int Iuc = oku ? Iu : 1, Irc = okr ? Ir : 1;  // clamped: every lane reads a valid cell
+                double bu, br_;
+                if constexpr (BM == 2) {  // rhs of the cells on diagonals d: TMEM column (d mod 256), warp-uniform
+                    uint32_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+                    if (du) tm_ld2(tq + 2u * uint32_t((bu0 - kLag * gu) & 255), lo0, hi0);
+                    if (dres) tm_ld2(tq + 2u * uint32_t((br0 - kLag * gr) & 255), lo1, hi1);
+                    tm_wait_ld();
+                    bu = __hiloint2double(int(hi0), int(lo0));
+                    br_ = __hiloint2double(int(hi1), int(lo1));
+                } else if constexpr (BM == 1) {
+                    bu = cl_dyn[browo + Iuc];
+                    br_ = cl_dyn[browo + Irc];
+                } else {
+                    bu = __ldg(brow + Iuc);
+                    br_ = __ldg(brow + Irc);
                 }
+                // both cells, branch-free, so their independent fp64 chains interleave
+                const Nbr vr = gather(rowo + Irc, pitch, true, T.five);
+                const Nbr vu = gather(rowo + Iuc, pitch, false, T.five);
+                const double rr = apply_std<true, Kind>(T, vr, br_);
+                const double out = apply_std<false, Kind>(T, vu, bu);
                 if (oku) {  // update of sweep gu
-                    double* p = rowp + Iu;
-                    const double bIJ = BSmem ? brow[Iu] : __ldg(brow + Iu);
-                    const double out = apply_std<false, Kind>(T, gather(p, pitch, false, T.five), bIJ);
-                    *p = out;
+                    cl_dyn[rowo + Iu] = out;
                     if (mirror_s) B.south[Iu] = out;
                     if (mirror_n) B.north[Iu] = out;
                 }
-                if (dres) {
+                if (dres) {  // residual of sweep gr (inputs final since step tau - 1)
+                    double m = okr ? fabs(rr) : 0.0;
+                    m = (m != m) ? 0.0 : m;  // std::max drops NaN
                     m = warp_max_nonneg(m);
                     if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
                 }
                 gu += kH, gr += kH;
             }
         }
-        // ---- ring cells: sweeps with a diagonal in [0, dmax], four lanes per sweep
-#pragma unroll 1
-        for (int phase = 0; phase < (residuals ? 2 : 1); ++phase) {
-            const int base = phase == 0 ? tau : tau - 4;
-            const int g_lo = max(0, (base - dmax + kLag - 1) >> 3), g_hi = min(G - 1, base >> 3);
-            const int g = g_lo + 8 * rw + rk;
-            if (base >= 0 && g_lo + 8 * rw <= g_hi) {
-                double m = 0.0;
-                if (g <= g_hi) {
-                    const int d = base - kLag * g;
-                    int I = -1, Jr = -1;
-                    if (side == 0) {  // first column (corners included)
-                        if ((d & 1) == 0) I = 0, Jr = d >> 1;
-                    } else if (side == 1) {  // last column (corners included)
-                        if (((d - T.ncx + 1) & 1) == 0) I = T.ncx - 1, Jr = (d - T.ncx + 1) >> 1;
-                    } else if (side == 2) {  // first row, corners excluded
-                        if (has_bottom && d >= 1 && d <= T.ncx - 2) I = d, Jr = 0;
-                    } else {  // last row, corners excluded
-                        const int It = d - 2 * (T.ncy - 1);
-                        if (has_top && It >= 1 && It <= T.ncx - 2) I = It, Jr = T.ncy - 1;
-                    }
-                    if (I >= 0 && Jr >= B.J0 && Jr < B.J1) m = ring_step<BSmem>(T, B, spec, cbg, I, Jr, phase == 1);
+        // ---- ring cells (first / last column and row) on their own warps: the
+        //      class-table stencil is a long chain, kept off the interior warps.
+        //      Column cells: lane = row; row cells: lanes over the sweeps in flight.
+#ifdef ISMG_CL_TRACE
+        const long long c1 = clock64();
+        tr_int += c1 - c0;
+#endif
+        if (ring_on) {
+            const int base = rph == 0 ? tau : tau - 4;
+            const bool res = rph == 1;
+            auto ring_max = [&](int g, double m) {  // per-sweep max of non-negative doubles
+                atomicMax(&cs.rmax[g], (unsigned long long)__double_as_longlong(m));
+            };
+            if (Jr < B.J1) {
+                // first column: d = 2J; last column: d = ncx - 1 + 2J
+                const int d0 = 2 * Jr, d1 = T.ncx - 1 + 2 * Jr;
+                if (base >= d0 && ((base - d0) & 7) == 0 && ((base - d0) >> 3) < G) {
+                    const double m = ring_step<BM>(T, B, cbg, 0, Jr, res);
+                    if (res) ring_max((base - d0) >> 3, m);
                 }
-                if (phase == 1) {  // max over the four sides of each sweep
-                    m = fmax(m, __shfl_xor_sync(kFull, m, 1));
-                    m = fmax(m, __shfl_xor_sync(kFull, m, 2));
-                    if (side == 0 && g <= g_hi) cs.rmax[g] = fmax(cs.rmax[g], m);
+                if (base >= d1 && ((base - d1) & 7) == 0 && ((base - d1) >> 3) < G) {
+                    const double m = ring_step<BM>(T, B, cbg, T.ncx - 1, Jr, res);
+                    if (res) ring_max((base - d1) >> 3, m);
+                }
+            }
+            // first / last row (corners excluded): the row block that holds them
+            const bool bot = has_bottom && rr == 0, top = has_top && B.J1 - 1 >= B.J0 + 32 * rr &&
+                                                                  B.J1 - 1 < B.J0 + 32 * rr + 32;
+            if (bot || top) {
+                const int Jrow = bot ? 0 : T.ncy - 1;
+                const int off = 2 * Jrow;  // cell (I, Jrow) on diagonal I + off
+                const int g_lo = max(0, (base - off - (T.ncx - 2) + kLag - 1) >> 3);
+                const int g_hi = min(G - 1, (base - off - 1) >> 3);
+#pragma unroll 1
+                for (int g = g_lo + lane; g <= g_hi; g += 32) {
+                    const int I = base - off - kLag * g;
+                    const double m = ring_step<BM>(T, B, cbg, I, Jrow, res);
+                    if (res) ring_max(g, m);
+                }
+                if (bot && top) {  // a single-block band holding both rows
+                    const int off2 = 2 * (T.ncy - 1);
+                    const int g_lo2 = max(0, (base - off2 - (T.ncx - 2) + kLag - 1) >> 3);
+                    const int g_hi2 = min(G - 1, (base - off2 - 1) >> 3);
+#pragma unroll 1
+                    for (int g = g_lo2 + lane; g <= g_hi2; g += 32) {
+                        const int I = base - off2 - kLag * g;
+                        const double m = ring_step<BM>(T, B, cbg, I, T.ncy - 1, res);
+                        if (res) ring_max(g, m);
+                    }
                 }
             }
         }
+#ifdef ISMG_CL_TRACE
+        const long long c2 = clock64();
+        tr_ring += c2 - c1;
+#endif
         step_sync(B);
+#ifdef ISMG_CL_TRACE
+        tr_bar += clock64() - c2;
+#endif
     }
+#ifdef ISMG_CL_TRACE
+    if (lane == 0 && G >= 4 && G <= 8 && residuals)
+        printf("TRACE G=%d steps=%d warp=%2d int=%lld ring=%lld bar=%lld per-step int=%.0f ring=%.0f bar=%.0f\n", G,
+               tau_end + 1, warp, tr_int, tr_ring, tr_bar, double(tr_int) / (tau_end + 1),
+               double(tr_ring) / (tau_end + 1), double(tr_bar) / (tau_end + 1));
+#endif
 }
 
-template <int Kind, bool BSmem>
+template <int Kind, int BM>
 __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom T, const double* spec_g,
                                                                double* backup) {
-    extern __shared__ __align__(16) double dyn[];
     __shared__ ClShared cs;
     Ctl* st = P.ctl;
     if (st->phase != kCoarse) return;
     const long long t_start = gtimer();
     cg::cluster_group cluster = cg::this_cluster();
+    double* dyn = cl_dyn;
     Band B;
     B.C = int(cluster.num_blocks());
     B.c = int(cluster.block_rank());
@@ -342,16 +427,42 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
     const int pitch = T.pitch;
     const int rows = R + 2;
     B.xs = dyn;
-    double* bsm = dyn + size_t(rows) * pitch;
+    B.bo = rows * pitch;
+    double* bsm = dyn + B.bo;
     B.bpitch = T.bpitch;
-    B.bs = bsm;
-    double* spec = bsm + (BSmem ? size_t(R) * T.bpitch : 0);
+    B.so = B.bo + (BM == 1 ? R * T.bpitch : 0);
+    double* spec = dyn + B.so;
     // mirrors: my row J0 is row (R + 1) of the CTA below's buffer; my row J1-1 is row 0 of the CTA above
     B.south = (B.c > 0) ? cluster.map_shared_rank(B.xs, B.c - 1) + size_t(R + 1) * pitch + 1 : nullptr;
     B.north = (B.c + 1 < B.C && B.J1 < T.ncy) ? cluster.map_shared_rank(B.xs, B.c + 1) + 1 : nullptr;
     const int nxs = rows * pitch;
     for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = 0.0;  // ce = 0, zero ghosts and halos
-    if (BSmem)
+    B.tmem = 0;
+    if constexpr (BM == 2) {  // rhs into Tensor Memory: 512 columns = 256 fp64 diagonal slots per row
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                uint32_t(__cvta_generic_to_shared(&cs.ictl[3]))));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+        B.tmem = uint32_t(cs.ictl[3]);
+        const int q = warp & 3, nh = int(blockDim.x >> 7);
+        const int J = B.J0 + 32 * q + lane;
+        const uint32_t tq = B.tmem + (uint32_t(32 * q) << 16);
+        for (int slot = warp >> 2; slot < 256; slot += nh) {
+            const int I = (slot - 2 * J) & 255;
+            const double v = (J < B.J1 && I < T.ncx) ? P.cb.at(I, J) : 0.0;
+            tm_st2(tq + 2u * uint32_t(slot), uint32_t(__double2loint(v)), uint32_t(__double2hiint(v)));
+        }
+        tm_wait_st();
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+    }
+    if (BM == 1)
         for (int k = threadIdx.x; k < (B.J1 - B.J0) * T.ncx; k += blockDim.x) {
             const int jj = k / T.ncx, I = k - jj * T.ncx;
             bsm[jj * T.bpitch + I] = P.cb.at(I, B.J0 + jj);
@@ -370,14 +481,14 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
         if (G > 1)
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) my_backup[k] = B.xs[k];  // checkpoint
         const long long tg0 = gtimer();
-        cl_group<Kind, BSmem>(T, B, spec, P.cb, cs, G, true);
+        cl_group<Kind, BM>(T, B, P.cb, cs, G, true);
         gns += gtimer() - tg0;
         steps += dmax + kLag * (G - 1) + 5;
         // cluster-wide first sweep whose residual passes tol_coarse
         {
             const int nrb = (B.J1 - B.J0 + 31) >> 5;
             for (int g = threadIdx.x; g < G; g += blockDim.x) {
-                double m = fmax(cs.cmax[0][g], cs.rmax[g]);
+                double m = fmax(cs.cmax[0][g], __longlong_as_double((long long)cs.rmax[g]));
                 for (int r = 1; r < nrb; ++r) m = fmax(m, cs.cmax[r][g]);
                 cs.gmax[g] = m;
             }
@@ -406,7 +517,7 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = my_backup[k];
             cluster.sync();
             const long long tg0 = gtimer();
-            cl_group<Kind, BSmem>(T, B, spec, P.cb, cs, first + 1, false);
+            cl_group<Kind, BM>(T, B, P.cb, cs, first + 1, false);
             gns += gtimer() - tg0;
             steps += dmax + kLag * first + 1;
             done += first + 1;
@@ -441,6 +552,12 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
         const int jj = k / T.ncx, I = k - jj * T.ncx;
         P.ce.at(I, B.J0 + jj) = B.xs[(jj + 1) * pitch + 1 + I];
     }
+    if constexpr (BM == 2) {
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+        if ((threadIdx.x >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(B.tmem));
+    }
     cluster.sync();  // no CTA exits while another may still read its shared memory
     if (B.c == 0 && threadIdx.x == 0) {
         st->coarse_launches += 1;
@@ -465,7 +582,7 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
 
 bool same_bits(double a, double b) { return a == b && std::signbit(a) == std::signbit(b); }
 
-template <int Kind, bool BSmem>
+template <int Kind, int BM>
 void launch_one(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(T.csize);
@@ -479,14 +596,14 @@ void launch_one(const Params& P, const ClGeom& T, const double* spec, double* ba
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    ISMG_CUDA(cudaLaunchKernelEx(&cfg, coarse_cl_kernel<Kind, BSmem>, P, T, spec, backup));
+    ISMG_CUDA(cudaLaunchKernelEx(&cfg, coarse_cl_kernel<Kind, BM>, P, T, spec, backup));
 }
 
-template <int Kind, bool BSmem>
+template <int Kind, int BM>
 void set_attrs(size_t smem) {
-    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
-    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BSmem>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    ISMG_CUDA(cudaFuncSetAttribute(coarse_cl_kernel<Kind, BM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 }  // namespace
@@ -556,19 +673,21 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     const size_t cap = 200 * 1024;
     const size_t spec_bytes = spec.size() * sizeof(double);
     // smallest cluster whose bands fit shared memory (a cluster barrier costs ~6x a
-    // CTA barrier): rhs in shared memory if it fits too, else read through L1
+    // CTA barrier); rhs in shared memory if it fits too, else in Tensor Memory
+    // (bands <= 128 rows, ncx <= 256), else read through L1
     for (int C = 1; C <= 16; C *= 2)
-        for (int bsm = 1; bsm >= 0; --bsm) {
+        for (int bm : {1, 2, 0}) {
             int R = (op.ncy + C - 1) / C;
             R = (R + 31) / 32 * 32;  // whole 32-row blocks
             if (R > 32 * kMaxRowBlocks) continue;
             if ((op.ncy + R - 1) / R < C) continue;  // no empty CTAs
-            const size_t bytes = (size_t(R + 2) * T.pitch + (bsm ? size_t(R) * T.bpitch : 0)) * sizeof(double) +
+            if (bm == 2 && (R > 128 || op.ncx > 256)) continue;
+            const size_t bytes = (size_t(R + 2) * T.pitch + (bm == 1 ? size_t(R) * T.bpitch : 0)) * sizeof(double) +
                                  spec_bytes;
             if (bytes <= cap) {
                 T.csize = (op.ncy + R - 1) / R;
                 T.band = R;
-                T.bsmem = bsm;
+                T.bsmem = bm;
                 smem = bytes;
                 return true;
             }
@@ -580,19 +699,25 @@ size_t cl_backup_doubles(const ClGeom& T) { return size_t(T.csize) * size_t(T.ba
 
 void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
                       cudaStream_t st) {
-    if (T.bsmem) {
-        if (T.kind == 1) launch_one<1, true>(P, T, spec, backup, smem, st);
-        else if (T.kind == 2) launch_one<2, true>(P, T, spec, backup, smem, st);
-        else launch_one<0, true>(P, T, spec, backup, smem, st);
+    const int k = T.kind, m = T.bsmem;
+    if (k == 1) {
+        if (m == 2) launch_one<1, 2>(P, T, spec, backup, smem, st);
+        else if (m == 1) launch_one<1, 1>(P, T, spec, backup, smem, st);
+        else launch_one<1, 0>(P, T, spec, backup, smem, st);
+    } else if (k == 2) {
+        if (m == 2) launch_one<2, 2>(P, T, spec, backup, smem, st);
+        else if (m == 1) launch_one<2, 1>(P, T, spec, backup, smem, st);
+        else launch_one<2, 0>(P, T, spec, backup, smem, st);
     } else {
-        if (T.kind == 1) launch_one<1, false>(P, T, spec, backup, smem, st);
-        else if (T.kind == 2) launch_one<2, false>(P, T, spec, backup, smem, st);
-        else launch_one<0, false>(P, T, spec, backup, smem, st);
+        if (m == 2) launch_one<0, 2>(P, T, spec, backup, smem, st);
+        else if (m == 1) launch_one<0, 1>(P, T, spec, backup, smem, st);
+        else launch_one<0, 0>(P, T, spec, backup, smem, st);
     }
 }
 void set_coarse_cl_smem(size_t bytes) {
-    set_attrs<0, true>(bytes), set_attrs<1, true>(bytes), set_attrs<2, true>(bytes);
-    set_attrs<0, false>(bytes), set_attrs<1, false>(bytes), set_attrs<2, false>(bytes);
+    set_attrs<0, 0>(bytes), set_attrs<1, 0>(bytes), set_attrs<2, 0>(bytes);
+    set_attrs<0, 1>(bytes), set_attrs<1, 1>(bytes), set_attrs<2, 1>(bytes);
+    set_attrs<0, 2>(bytes), set_attrs<1, 2>(bytes), set_attrs<2, 2>(bytes);
 }
 
 }  // namespace fz

@@ -296,7 +296,7 @@ struct ClGeom {
     int ncx, ncy;
     int pitch, bpitch;  // shared-memory row pitches (3 mod 16 doubles)
     int csize, band;    // cluster size (CTAs), rows per CTA band
-    int bsmem;          // rhs band in shared memory (else read through L1)
+    int bsmem;          // rhs: 1 shared memory, 2 Tensor Memory, 0 read through L1
     int ring, ncls, fastdiv, kind;
     bool five;
     double stdw[9];
