@@ -29,6 +29,10 @@ namespace fz {
 
 namespace {
 
+#ifndef ISMG_FINE_MINB
+#define ISMG_FINE_MINB 1  // minimum resident CTAs per SM requested from ptxas (register cap)
+#endif
+
 constexpr int kRowW = 128;  // ring row: columns [a-4, a+124)
 constexpr int kRingW = 6;   // rows in flight
 
@@ -118,16 +122,19 @@ __device__ __forceinline__ void halo_geo(Geo& G, const Params& P, int c0) {
     if (P.row1 < P.ny) G.hs1 = P.halo_send[1] + kXOff + c0, G.hj1 = P.row1 - 3;
 }
 
-// store a finished quad row j (and its halo copy for the neighbour rank)
+// store a finished quad row j (multi-GPU: and its halo copy for the neighbour rank)
+template <bool MP>
 __device__ __forceinline__ void put_row(const Geo& G, const Lane& L, int j, const double* v) {
     double* dst = G.outp + int64_t(j) * G.pitch;
     double* hs = nullptr;
-    if (unsigned(j - G.hj0) < 3u) hs = G.hs0 + int64_t(j - G.hj0) * G.pitch;
-    if (unsigned(j - G.hj1) < 3u) hs = G.hs1 + int64_t(j - G.hj1) * G.pitch;
+    if constexpr (MP) {
+        if (unsigned(j - G.hj0) < 3u) hs = G.hs0 + int64_t(j - G.hj0) * G.pitch;
+        if (unsigned(j - G.hj1) < 3u) hs = G.hs1 + int64_t(j - G.hj1) * G.pitch;
+    }
     if (!L.spec) {
         reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
         reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
-        if (hs) {
+        if (MP && hs) {
             reinterpret_cast<double2*>(hs)[0] = make_double2(v[0], v[1]);
             reinterpret_cast<double2*>(hs)[1] = make_double2(v[2], v[3]);
         }
@@ -136,7 +143,7 @@ __device__ __forceinline__ void put_row(const Geo& G, const Lane& L, int j, cons
         for (int q = 0; q < 4; ++q)
             if (L.dom[q]) {
                 dst[q] = v[q];
-                if (hs) hs[q] = v[q];
+                if (MP && hs) hs[q] = v[q];
             }
     }
 }
@@ -154,7 +161,7 @@ __device__ __forceinline__ double gs_exact(double W, double E, double S, double 
 }
 
 // Iteration k; row k-1 has parity P1.
-template <int U, int P1>
+template <int U, int P1, bool MP>
 __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L, const Geo& G, Win& w, Acc& A, int k) {
     constexpr int s0 = U, s1 = (U + 3) & 3, s2 = (U + 2) & 3, s3 = (U + 1) & 3;
     const int si = 4 * L.l;
@@ -243,7 +250,7 @@ __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L,
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));  // std::max(rmax, |r|): NaN dropped
             A.sx = A.sx + ((x3[0] + x3[1]) + (x3[2] + x3[3]));   // out-of-domain cells hold 0
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            put_row(G, L, j, x3);
+            put_row<MP>(G, L, j, x3);
         }
     }
     // row k takes the slot of row k-4
@@ -309,6 +316,7 @@ __device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double 
 
 __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
+template <bool MP>
 __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& st, int nq) {
     const int W = 4 * nq;
     const int a = blockIdx.x * W;
@@ -319,11 +327,14 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
-    halo_geo(G, P, L.c0);
+    if (MP) halo_geo(G, P, L.c0);
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
+    auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
+        return MP ? row_src(P, xin, k, a - 4) : xin + int64_t(k) * G.pitch + (a - 4);
+    };
     const int kfirst = G.r0 - 3, klast = G.r1 + 2;
     if ((threadIdx.x & 31) == 0) {
         for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
@@ -331,7 +342,7 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     }
     __syncwarp();
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
-        issue_row_w(sm, row_src(P, xin, kfirst + s, a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+        issue_row_w(sm, xsrc(kfirst + s), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     Win w;
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -344,12 +355,12 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     auto row = [&](auto u, int k) {
         constexpr int U = decltype(u)::value;
         mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
-        step_w<U, (U & 1)>(sm, slot, L, G, w, A, k);
+        step_w<U, (U & 1), MP>(sm, slot, L, G, w, A, k);
         const int j = k - 3;  // tile row-block of row k-3 complete
         if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
         __syncwarp();  // every lane has read the slot of row k
         if (k + kRingW <= klast)
-            issue_row_w(sm, row_src(P, xin, k + kRingW, a - 4), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
+            issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     };
     // kfirst = r0 - 3 = 1 (mod 4) (P.H is a multiple of 4), so in the block
@@ -366,6 +377,7 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
 // ---- PROLONG / RESID: x' = x + c + P ce (coarsening.hpp:495-500), residual and
 // restriction of x'. Iteration k loads (and prolongs) row k and forms the
 // residual of row k-1 with rows k-2, k-1 in registers.
+template <bool MP>
 __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl& st, int nq, bool prolong) {
     const int W = 4 * nq;
     const int a = blockIdx.x * W;
@@ -376,11 +388,14 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
-    halo_geo(G, P, L.c0);
+    if (MP) halo_geo(G, P, L.c0);
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
+    auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
+        return MP ? row_src(P, xin, k, a - 4) : xin + int64_t(k) * G.pitch + (a - 4);
+    };
     Acc A;
     // TileAxis::locate_cell of the lane's columns
     int I0[4], I1[4];
@@ -400,7 +415,7 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     }
     __syncwarp();
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
-        issue_row_w(sm, row_src(P, xin, kfirst + s, a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+        issue_row_w(sm, xsrc(kfirst + s), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     const uint32_t bar0 = su32(&sm.bar[0]);
     double x1[4] = {0, 0, 0, 0}, x2[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
     int slot = 0;
@@ -450,25 +465,26 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
             A.sx = A.sx + ((x1[0] + x1[1]) + (x1[2] + x1[3]));
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            if (prolong) put_row(G, L, j, x1);
+            if (prolong) put_row<MP>(G, L, j, x1);
         }
         if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
 #pragma unroll
         for (int q = 0; q < 4; ++q) x2[q] = x1[q], x1[q] = x0[q], b1[q] = b0[q];
         __syncwarp();
         if (k + kRingW <= klast)
-            issue_row_w(sm, row_src(P, xin, k + kRingW, a - 4), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
+            issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     }
     warp_epilogue(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan);
 }
 
-__global__ void __launch_bounds__(32) fine_pass_w_kernel(Params P, int nq) {
+template <bool MP>
+__global__ void __launch_bounds__(32, ISMG_FINE_MINB) fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
-    if (st.phase == kFine) sweep_w(sm, P, st, nq);
-    else if (st.phase == kProlong) prolong_w(sm, P, st, nq, true);
-    else if (st.phase == kResid) prolong_w(sm, P, st, nq, false);
+    if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
+    else if (st.phase == kProlong) prolong_w<MP>(sm, P, st, nq, true);
+    else if (st.phase == kResid) prolong_w<MP>(sm, P, st, nq, false);
 }
 
 }  // namespace
@@ -485,7 +501,8 @@ dim3 fine_pass_w_grid(const Params& P) {
     return dim3((P.nx + W - 1) / W, P.nchunks);
 }
 void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st) {
-    fine_pass_w_kernel<<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
+    if (P.mp) fine_pass_w_kernel<true><<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
+    else fine_pass_w_kernel<false><<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
 }
 
 }  // namespace fz
