@@ -272,38 +272,62 @@ __device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int
     A.tacc = 0.0;
 }
 
-// Warp-level epilogue: one partial triple per warp (= CTA); the last warp to
-// finish reduces them and applies the reference's branch logic.
+// Warp-level epilogue, a fixed two-level tree (deterministic sums): every warp
+// (= CTA) stores its partial triple; the last warp of each group of 32 CTAs
+// folds the group (one partial per lane); the last group folds the group
+// partials and applies the reference's branch logic. (A single final warp
+// folding all ~5500 partials serially added a multi-microsecond tail to every
+// pass.) Scratch: part = [3 per CTA | 3 per group], ticket = [all | per group].
 __device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double mx, double sx, double cm, int nan) {
     const int nb = gridDim.x * gridDim.y;
     const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int ng = (nb + 31) >> 5, grp = bid >> 5;
+    double* gpart = P.part + 3 * nb;
     mx = warp_max(mx);
     sx = warp_sum_down(sx);
     cm = warp_max(cm);
     const int anynan = __any_sync(kFull, nan);
     unsigned last = 0;
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         P.part[3 * bid] = mx;
         P.part[3 * bid + 1] = sx;
         P.part[3 * bid + 2] = cm;
         if (anynan) P.ctl->nan_seen = 1;
         __threadfence();
-        last = atomicAdd(P.ticket, 1u) == unsigned(nb - 1);
+        const unsigned gsize = unsigned(min(32, nb - 32 * grp));
+        last = atomicAdd(&P.ticket[1 + grp], 1u) == gsize - 1;
     }
-    last = __shfl_sync(kFull, last, 0);
-    if (!last) return;
+    if (!__shfl_sync(kFull, last, 0)) return;
+    __threadfence();
+    {  // fold the group: member 32 grp + lane
+        const int k = 32 * grp + lane;
+        double m = 0.0, s = 0.0, c = 0.0;
+        if (k < nb) m = __ldcg(&P.part[3 * k]), s = __ldcg(&P.part[3 * k + 1]), c = __ldcg(&P.part[3 * k + 2]);
+        m = warp_max(m);
+        s = warp_sum_down(s);
+        c = warp_max(c);
+        last = 0;
+        if (lane == 0) {
+            gpart[3 * grp] = m, gpart[3 * grp + 1] = s, gpart[3 * grp + 2] = c;
+            P.ticket[1 + grp] = 0u;
+            __threadfence();
+            last = atomicAdd(P.ticket, 1u) == unsigned(ng - 1);
+        }
+    }
+    if (!__shfl_sync(kFull, last, 0)) return;
     __threadfence();
     double m = 0.0, s = 0.0, c = 0.0;
-    for (int k = threadIdx.x & 31; k < nb; k += 32) {
-        m = fmax(m, __ldcg(&P.part[3 * k]));
-        s += __ldcg(&P.part[3 * k + 1]);
-        c = fmax(c, __ldcg(&P.part[3 * k + 2]));
+    for (int k = lane; k < ng; k += 32) {
+        m = fmax(m, __ldcg(&gpart[3 * k]));
+        s += __ldcg(&gpart[3 * k + 1]);
+        c = fmax(c, __ldcg(&gpart[3 * k + 2]));
     }
     m = warp_max(m);
     s = warp_sum_down(s);
     c = warp_max(c);
-    if ((threadIdx.x & 31) == 0) {
-        if (P.mp) {  // all-reduced across ranks, then mp_decide_kernel
+    if (lane == 0) {
+        if (P.mp) {  // all-reduced across ranks, then mp_unpack_kernel decides
             P.rank_part[0] = m, P.rank_part[1] = c, P.rank_part[2] = 1.0, P.rank_part[3] = double(mode);
             P.rank_part[4] = s;
         } else {
