@@ -34,6 +34,9 @@
 #include "fused_impl.cuh"
 
 namespace cg = cooperative_groups;
+#ifndef ISMG_CL_TRACE_WARPS
+#define ISMG_CL_TRACE_WARPS 1
+#endif
 
 namespace ismgb {
 namespace fz {
@@ -43,9 +46,8 @@ namespace {
 constexpr int kLag = 8;            // wavefront steps between consecutive sweeps
 constexpr int kMaxGroup = 512;     // sweeps per checkpointed group
 constexpr int kPredCap = 32;       // cap of the predicted first group of a visit
-constexpr int kIntWarps = 16;                  // warps relaxing interior cells
-constexpr int kRingWarps = 8;                  // warps relaxing ring cells: (row block, phase)
-constexpr int kClThreads = 32 * (kIntWarps + kRingWarps);
+constexpr int kIntWarps = 16;     // warps: 4 row blocks x 4 sweeps in flight
+constexpr int kClThreads = 32 * kIntWarps;
 
 constexpr int kMaxRowBlocks = 4;  // 32-row blocks per CTA band
 
@@ -55,20 +57,12 @@ extern __shared__ __align__(16) double cl_dyn[];
 
 struct ClShared {
     double cmax[kMaxRowBlocks][kMaxGroup];  // residual max per (row block, sweep of the group)
-    unsigned long long rmax[kMaxGroup];     // residual max of the ring cells per sweep (double bits)
     double gmax[kMaxGroup];                 // ... all reduced over the CTA
     double red[32];
     double bcast[4];
     int ictl[4];
     int first;
 };
-
-__device__ __forceinline__ int ring_index(const ClGeom& T, int I, int J) {
-    if (J == 0) return I;
-    if (J == T.ncy - 1) return T.ncx + I;
-    if (I == 0) return 2 * T.ncx + J;
-    return 2 * T.ncx + T.ncy + J;
-}
 
 struct Nbr {
     double c, e, w, n, s, ne, nw, se, sw;
@@ -91,86 +85,6 @@ __device__ __forceinline__ Nbr gather(int o, int pitch, bool with_c, bool five) 
         v.ne = v.nw = v.se = v.sw = 0.0;
     }
     return v;
-}
-
-// Reference order (coarsening.hpp:539-543 residual, :558-565 update): slots
-// E, W, N, S, NE, NW, SE, SW, each skipped when its weight is zero.
-template <bool kResidual>
-__device__ __forceinline__ double apply_w(const double* w, const Nbr& v, double bIJ, bool five) {
-    double acc = kResidual ? w[0] * v.c : 0.0;
-    if (w[1] != 0.0) acc += w[1] * v.e;
-    if (w[2] != 0.0) acc += w[2] * v.w;
-    if (w[3] != 0.0) acc += w[3] * v.n;
-    if (w[4] != 0.0) acc += w[4] * v.s;
-    if (!five) {
-        if (w[5] != 0.0) acc += w[5] * v.ne;
-        if (w[6] != 0.0) acc += w[6] * v.nw;
-        if (w[7] != 0.0) acc += w[7] * v.se;
-        if (w[8] != 0.0) acc += w[8] * v.sw;
-    }
-    return kResidual ? bIJ - acc : (bIJ - acc) / w[0];
-}
-
-// a / -3 correctly rounded by Markstein's correction (y = RN(-1/3); checked
-// against __ddiv_rn on 1.2e9 operands, tools/verify_div3.cu)
-__device__ __forceinline__ double div_m3(double a) {
-    constexpr double y = -1.0 / 3.0;
-    const double q = __dmul_rn(a, y);
-    const double r = __fma_rn(-q, -3.0, a);
-    return __fma_rn(r, y, q);
-}
-
-template <bool kResidual, int Kind>
-__device__ __forceinline__ double apply_std(const ClGeom& T, const Nbr& v, double bIJ) {
-    if constexpr (Kind == 1) {  // ISMG interior: C -3, E/W/N/S 1/2, corners 1/4
-        double acc = kResidual ? -3.0 * v.c : 0.0;
-        acc += 0.5 * v.e;
-        acc += 0.5 * v.w;
-        acc += 0.5 * v.n;
-        acc += 0.5 * v.s;
-        acc += 0.25 * v.ne;
-        acc += 0.25 * v.nw;
-        acc += 0.25 * v.se;
-        acc += 0.25 * v.sw;
-        return kResidual ? bIJ - acc : div_m3(bIJ - acc);
-    } else if constexpr (Kind == 2) {  // five-point interior: C -4, E/W/N/S 1
-        double acc = kResidual ? -4.0 * v.c : 0.0;
-        acc += 1.0 * v.e;
-        acc += 1.0 * v.w;
-        acc += 1.0 * v.n;
-        acc += 1.0 * v.s;
-        return kResidual ? bIJ - acc : (bIJ - acc) * -0.25;  // exact: power-of-two divisor
-    } else {
-        return apply_w<kResidual>(T.stdw, v, bIJ, T.five);
-    }
-}
-
-// boundary-ring cell: 9 weights + RN(1/w0) of its class (spec table in smem)
-template <bool kResidual>
-__device__ __forceinline__ double ring_cell(const ClGeom& T, int so, const Nbr& v, int I, int J, double bIJ) {
-    const int* ring_cls = reinterpret_cast<const int*>(cl_dyn + so + 10 * T.ncls);
-    const double* wc = cl_dyn + so + 10 * ring_cls[ring_index(T, I, J)];
-    double w[9];
-#pragma unroll
-    for (int sl = 0; sl < 9; ++sl) w[sl] = wc[sl];
-    if (kResidual) return apply_w<true>(w, v, bIJ, T.five);
-    double acc = 0.0;  // update: coarsening.hpp:558-565
-    if (w[1] != 0.0) acc += w[1] * v.e;
-    if (w[2] != 0.0) acc += w[2] * v.w;
-    if (w[3] != 0.0) acc += w[3] * v.n;
-    if (w[4] != 0.0) acc += w[4] * v.s;
-    if (!T.five) {
-        if (w[5] != 0.0) acc += w[5] * v.ne;
-        if (w[6] != 0.0) acc += w[6] * v.nw;
-        if (w[7] != 0.0) acc += w[7] * v.se;
-        if (w[8] != 0.0) acc += w[8] * v.sw;
-    }
-    const double num = bIJ - acc;
-    if (!T.fastdiv) return num / w[0];
-    const double y = wc[9];  // Markstein: exact RN(num / w0) (host-verified per class)
-    const double q = __dmul_rn(num, y);
-    const double r = __fma_rn(-q, w[0], num);
-    return __fma_rn(r, y, q);
 }
 
 // max over the warp of non-negative doubles (their order = the order of the
@@ -210,83 +124,123 @@ __device__ __forceinline__ void step_sync(const Band& B) {
     else __syncthreads();
 }
 
-// One group of G sweeps (residuals: also form the residual max of every sweep).
-// One ring cell (boundary row or column) of sweep g at its step: update or residual.
-template <int BM>
-__device__ __forceinline__ double ring_step(const ClGeom& T, const Band& B, const View& cbg, int I, int J,
-                                            bool residual) {
-    const int o = (J - B.J0 + 1) * T.pitch + 1 + I;
-    const double bIJ = BM == 1 ? cl_dyn[B.bo + (J - B.J0) * B.bpitch + I] : __ldg(&cbg.p[int64_t(J) * cbg.pitch + I]);
-    const Nbr v = gather(o, T.pitch, residual, T.five);
-    if (residual) {
-        const double m = fabs(ring_cell<true>(T, B.so, v, I, J, bIJ));
-        return (m != m) ? 0.0 : m;  // std::max drops NaN
+// Weights of one cell in slot order C, E, W, N, S, NE, NW, SE, SW; y = RN(1 / w[0]).
+struct Wts {
+    double w[9], y;
+};
+__device__ __forceinline__ void load_wts(int off, Wts& W) {  // off even: 16-byte loads
+    const double2* p = reinterpret_cast<const double2*>(cl_dyn + off);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const double2 v = p[k];
+        if (2 * k < 9) W.w[2 * k] = v.x;
+        if (2 * k + 1 < 9) W.w[2 * k + 1] = v.y;
+        else W.y = v.y;
     }
-    const double out = ring_cell<false>(T, B.so, v, I, J, bIJ);
-    cl_dyn[o] = out;
-    if (J == B.J0 && B.south != nullptr) B.south[I] = out;
-    if (J == B.J1 - 1 && B.north != nullptr) B.north[I] = out;
-    return 0.0;
+}
+
+// Term of one slot. The reference skips a zero weight's slot (coarsening.hpp:
+// 539-543 residual, :558-565 update). When every zero weight faces a ghost
+// (value +0.0), w * v is a signed zero, an exact identity of the update's sum
+// (it starts at +0.0, so it is never -0.0) and at most flips the sign of a
+// zero residual, whose |r| is all that is used: kSel = false multiplies
+// straight through. Otherwise (kSel) the slot's term is -0.0, the identity of +.
+template <bool kSel>
+__device__ __forceinline__ double term(double w, double v) {
+    if constexpr (kSel) return w != 0.0 ? w * v : -0.0;
+    return w * v;
+}
+
+// Update (num / w0) or residual (b - A x) of one cell with per-lane weights.
+template <bool kResidual, bool kFive, bool kSel>
+__device__ __forceinline__ double apply_lane(const Wts& W, const Nbr& v, double bIJ, bool fastdiv) {
+    double acc = kResidual ? W.w[0] * v.c : 0.0;
+    acc += term<kSel>(W.w[1], v.e);
+    acc += term<kSel>(W.w[2], v.w);
+    acc += term<kSel>(W.w[3], v.n);
+    acc += term<kSel>(W.w[4], v.s);
+    if (!kFive) {
+        acc += term<kSel>(W.w[5], v.ne);
+        acc += term<kSel>(W.w[6], v.nw);
+        acc += term<kSel>(W.w[7], v.se);
+        acc += term<kSel>(W.w[8], v.sw);
+    }
+    const double num = bIJ - acc;
+    if (kResidual) return num;
+    if (!fastdiv) return num / W.w[0];
+    const double q = __dmul_rn(num, W.y);  // Markstein: exact RN(num / w0) (host-verified per divisor)
+    const double r = __fma_rn(-q, W.w[0], num);
+    return __fma_rn(r, W.y, q);
 }
 
 // One group of G sweeps (residuals: also form the residual max of every sweep).
-// Interior cells: lane = row J, warps of a row block split the sweeps in
-// flight (g = h mod kH). Ring cells (first / last row and column) run on
-// their own warps, one per (row block, phase), so the interior warps never
-// diverge on them and the class-table chain stays off their critical path.
+// Lane = row J of a 32-row block; the warps of a row block split the sweeps in
+// flight (g = h mod kH). Sweep g updates diagonal I + 2J = tau - 8g at step tau
+// and forms its residual on tau - 4 - 8g; one loop iteration carries one of
+// each, so their independent fp64 chains overlap. Every lane keeps the weights
+// of its current update and residual cells in registers and reloads them from
+// the class table only when the cell's class changes (ring cells: first / last
+// row and column; the interior is class ncls), so ring cells cost no extra pass.
 template <int Kind, int BM>
 __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G, bool residuals) {
+    constexpr bool kFive = (Kind & 1) != 0, kSel = (Kind & 2) != 0;
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = kIntWarps;
     const int nrb = (B.J1 - B.J0 + 31) >> 5;  // 32-row blocks of the band (1, 2 or 4)
     // TMEM rhs: a warp may only read its own lane quadrant, so row block = warp mod 4
     const int nq = BM == 2 ? 4 : nrb;
-    // warps per row block (power of two; nrb = 3 idles some). Measured (per-warp
-    // clock64 trace, ISMG_CL_TRACE): one cell-pair iteration is a ~500-cycle
-    // dependent chain, so the sweeps in flight are spread over all warps even when
-    // few are in flight (one warp per row block doubled the step time).
-    const int kH = 1 << (31 - __clz(nwarps / nq));
+    // warps per row block (power of two; nrb = 3 idles some). One cell-pair
+    // iteration is a long dependent chain, so the sweeps in flight are spread
+    // over all warps even when few are in flight.
+    const int kH = 1 << (31 - __clz(kIntWarps / nq));
     const int rb = warp % nq, h = warp / nq;
     const int Jw = B.J0 + 32 * rb;  // first row of the warp
     const int J = Jw + lane;
     const int jlast = min(Jw + 31, B.J1 - 1);
-    const bool is_int = warp < kIntWarps;
-    const bool rowint = is_int && rb < nrb && h < kH && J <= jlast && J > 0 && J < T.ncy - 1;  // interior row
+    const bool w_on = rb < nrb && h < kH;
+    const bool rowin = w_on && J <= jlast;  // this lane's row lies in the band
+    const bool ringrow = J == 0 || J == T.ncy - 1;
     const int pitch = T.pitch;
     // offsets of cell (0, J) of this lane's row (rows outside the band read row J0)
-    const int Jc = (J >= B.J0 && J < B.J1) ? J : B.J0;
+    const int Jc = rowin ? J : B.J0;
     const int rowo = (Jc - B.J0 + 1) * pitch + 1;
     const int browo = B.bo + (Jc - B.J0) * B.bpitch;
     const double* brow = cbg.p + int64_t(Jc) * cbg.pitch;
     const uint32_t tq = B.tmem + (uint32_t(32 * rb) << 16);  // TMEM lane quadrant of this warp (BM == 2)
-    const bool mirror_s = J == B.J0 && B.south != nullptr;
-    const bool mirror_n = J == B.J1 - 1 && B.north != nullptr;
-    const unsigned nint = unsigned(T.ncx - 2);  // interior columns 1..ncx-2
-    const bool has_bottom = B.J0 == 0, has_top = B.J1 == T.ncy;
+    const bool mirror_s = rowin && J == B.J0 && B.south != nullptr;
+    const bool mirror_n = rowin && J == B.J1 - 1 && B.north != nullptr;
+    const unsigned ncx = unsigned(T.ncx);
+    const bool fastdiv = T.fastdiv != 0;
+    // class table: 10 doubles per class (interior = class ncls), then the ring's class ids
+    const int icls = T.ncls;
+    const int* ring_cls = reinterpret_cast<const int*>(cl_dyn + B.so + 10 * (T.ncls + 1));
+    // table offsets of this lane's classes: interior, first / last column of its
+    // row; a first / last row's cells look theirs up by column (ring order:
+    // row 0 by I, row ncy-1 by ncx + I, column 0 by 2 ncx + J, column ncx-1 by
+    // 2 ncx + ncy + J)
+    const int rbase = J == 0 ? 0 : T.ncx;
+    const int off_i = B.so + 10 * icls;
+    const int off_w = rowin && !ringrow ? B.so + 10 * ring_cls[2 * T.ncx + J] : off_i;
+    const int off_e = rowin && !ringrow ? B.so + 10 * ring_cls[2 * T.ncx + T.ncy + J] : off_i;
     if (residuals) {
         for (int k = threadIdx.x; k < nrb * kMaxGroup; k += blockDim.x) (&cs.cmax[0][0])[k] = 0.0;
-        for (int k = threadIdx.x; k < kMaxGroup; k += blockDim.x) cs.rmax[k] = 0ull;
     }
     __syncthreads();
     const int tau_end = dmax + kLag * (G - 1) + (residuals ? 4 : 0);
     const int dlo = 2 * Jw, dhi = 2 * jlast + T.ncx - 1;
-    const bool int_on = is_int && rb < nrb && h < kH;
-    // ring warp: row block rr of the band, one phase (0 update, 1 residual)
-    const int rr = (warp - kIntWarps) >> 1, rph = (warp - kIntWarps) & 1;
-    const bool ring_on = !is_int && rr < nrb && (rph == 0 || residuals);
-    const int Jr = B.J0 + 32 * rr + lane;  // this ring lane's row
+    // G <= kH: every warp of a row block owns at most one sweep (g = h) for the
+    // whole group, so its residual max stays in a register until the group ends
+    const bool one_g = G <= kH;
+    double lmax = 0.0;
 #ifdef ISMG_CL_TRACE
-    long long tr_int = 0, tr_ring = 0, tr_bar = 0;
+    long long tr_int = 0, tr_bar = 0;
+    const long long tr_l0 = clock64();
 #endif
     for (int tau = 0; tau <= tau_end; ++tau) {
 #ifdef ISMG_CL_TRACE
         const long long c0 = clock64();
 #endif
-        // ---- interior cells of this warp's rows: updates on diagonals tau - 8g,
-        //      residuals on tau - 4 - 8g; one loop carries one of each, so the two
-        //      independent dependency chains overlap
-        if (int_on) {
+        if (w_on) {
             const int bu0 = tau, br0 = residuals ? tau - 4 : -1;
             int gu = 0, guh = -1, gr = 0, grh = -1;
             if (bu0 >= dlo) {
@@ -304,10 +258,22 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
             while (gu <= guh || gr <= grh) {
                 const bool du = gu <= guh, dres = gr <= grh;
                 const int Iu = Iu0 - kLag * gu, Ir = Ir0 - kLag * gr;
-                const bool oku = du && rowint && unsigned(Iu - 1) < nint;
-                const bool okr = dres && rowint && unsigned(Ir - 1) < nint;
-                const int Iuc = oku ? Iu : 1, Irc = okr ? Ir : 1;  // clamped: every lane reads a valid cell
+                const bool oku = du && rowin && unsigned(Iu) < ncx;
+                const bool okr = dres && rowin && unsigned(Ir) < ncx;
+                const int Iuc = oku ? Iu : 0, Irc = okr ? Ir : 0;  // clamped: every lane reads a valid cell
+                // weights of the two cells: interior, first / last column, or (first /
+                // last row) by column from the ring's class ids
+                const int offu = ringrow ? B.so + 10 * ring_cls[rbase + Iuc]
+                                         : (Iu == 0 ? off_w : Iu == T.ncx - 1 ? off_e : off_i);
+                const int offr = ringrow ? B.so + 10 * ring_cls[rbase + Irc]
+                                         : (Ir == 0 ? off_w : Ir == T.ncx - 1 ? off_e : off_i);
+                Wts Wu, Wr;
+                load_wts(offu, Wu);
+                load_wts(offr, Wr);
                 double bu, br_;
+#ifdef X_NOTMEM
+                if (true) { bu = 0.1; br_ = 0.2; } else
+#endif
                 if constexpr (BM == 2) {  // rhs of the cells on diagonals d: TMEM column (d mod 256), warp-uniform
                     uint32_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
                     if (du) tm_ld2(tq + 2u * uint32_t((bu0 - kLag * gu) & 255), lo0, hi0);
@@ -323,95 +289,54 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
                     br_ = __ldg(brow + Irc);
                 }
                 // both cells, branch-free, so their independent fp64 chains interleave
-                const Nbr vr = gather(rowo + Irc, pitch, true, T.five);
-                const Nbr vu = gather(rowo + Iuc, pitch, false, T.five);
-                const double rr = apply_std<true, Kind>(T, vr, br_);
-                const double out = apply_std<false, Kind>(T, vu, bu);
+                const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
+                const Nbr vu = gather(rowo + Iuc, pitch, false, kFive);
+                const double rres = apply_lane<true, kFive, kSel>(Wr, vr, br_, fastdiv);
+                const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
                 if (oku) {  // update of sweep gu
                     cl_dyn[rowo + Iu] = out;
+#ifndef X_NOMIRROR
                     if (mirror_s) B.south[Iu] = out;
                     if (mirror_n) B.north[Iu] = out;
+#endif
                 }
                 if (dres) {  // residual of sweep gr (inputs final since step tau - 1)
-                    double m = okr ? fabs(rr) : 0.0;
+                    double m = okr ? fabs(rres) : 0.0;
                     m = (m != m) ? 0.0 : m;  // std::max drops NaN
-                    m = warp_max_nonneg(m);
-                    if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
+                    if (one_g) {  // the warp's only sweep: keep a per-lane max, fold once per group
+                        lmax = fmax(lmax, m);
+                    } else {
+                        m = warp_max_nonneg(m);
+                        if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
+                    }
                 }
                 gu += kH, gr += kH;
             }
         }
-        // ---- ring cells (first / last column and row) on their own warps: the
-        //      class-table stencil is a long chain, kept off the interior warps.
-        //      Column cells: lane = row; row cells: lanes over the sweeps in flight.
 #ifdef ISMG_CL_TRACE
         const long long c1 = clock64();
         tr_int += c1 - c0;
 #endif
-        if (ring_on) {
-            const int base = rph == 0 ? tau : tau - 4;
-            const bool res = rph == 1;
-            auto ring_max = [&](int g, double m) {  // per-sweep max of non-negative doubles
-                atomicMax(&cs.rmax[g], (unsigned long long)__double_as_longlong(m));
-            };
-            if (Jr < B.J1) {
-                // first column: d = 2J; last column: d = ncx - 1 + 2J
-                const int d0 = 2 * Jr, d1 = T.ncx - 1 + 2 * Jr;
-                if (base >= d0 && ((base - d0) & 7) == 0 && ((base - d0) >> 3) < G) {
-                    const double m = ring_step<BM>(T, B, cbg, 0, Jr, res);
-                    if (res) ring_max((base - d0) >> 3, m);
-                }
-                if (base >= d1 && ((base - d1) & 7) == 0 && ((base - d1) >> 3) < G) {
-                    const double m = ring_step<BM>(T, B, cbg, T.ncx - 1, Jr, res);
-                    if (res) ring_max((base - d1) >> 3, m);
-                }
-            }
-            // first / last row (corners excluded): the row block that holds them
-            const bool bot = has_bottom && rr == 0, top = has_top && B.J1 - 1 >= B.J0 + 32 * rr &&
-                                                                  B.J1 - 1 < B.J0 + 32 * rr + 32;
-            if (bot || top) {
-                const int Jrow = bot ? 0 : T.ncy - 1;
-                const int off = 2 * Jrow;  // cell (I, Jrow) on diagonal I + off
-                const int g_lo = max(0, (base - off - (T.ncx - 2) + kLag - 1) >> 3);
-                const int g_hi = min(G - 1, (base - off - 1) >> 3);
-#pragma unroll 1
-                for (int g = g_lo + lane; g <= g_hi; g += 32) {
-                    const int I = base - off - kLag * g;
-                    const double m = ring_step<BM>(T, B, cbg, I, Jrow, res);
-                    if (res) ring_max(g, m);
-                }
-                if (bot && top) {  // a single-block band holding both rows
-                    const int off2 = 2 * (T.ncy - 1);
-                    const int g_lo2 = max(0, (base - off2 - (T.ncx - 2) + kLag - 1) >> 3);
-                    const int g_hi2 = min(G - 1, (base - off2 - 1) >> 3);
-#pragma unroll 1
-                    for (int g = g_lo2 + lane; g <= g_hi2; g += 32) {
-                        const int I = base - off2 - kLag * g;
-                        const double m = ring_step<BM>(T, B, cbg, I, T.ncy - 1, res);
-                        if (res) ring_max(g, m);
-                    }
-                }
-            }
-        }
-#ifdef ISMG_CL_TRACE
-        const long long c2 = clock64();
-        tr_ring += c2 - c1;
-#endif
         step_sync(B);
 #ifdef ISMG_CL_TRACE
-        tr_bar += clock64() - c2;
+        tr_bar += clock64() - c1;
 #endif
     }
+    if (one_g && residuals && w_on && h < G) {  // fold the per-lane maxima of sweep h
+        const double m = warp_max_nonneg(lmax);
+        if (lane == 0) cs.cmax[rb][h] = fmax(cs.cmax[rb][h], m);
+    }
+    __syncthreads();
 #ifdef ISMG_CL_TRACE
-    if (lane == 0 && G >= 4 && G <= 8 && residuals)
-        printf("TRACE G=%d steps=%d warp=%2d int=%lld ring=%lld bar=%lld per-step int=%.0f ring=%.0f bar=%.0f\n", G,
-               tau_end + 1, warp, tr_int, tr_ring, tr_bar, double(tr_int) / (tau_end + 1),
-               double(tr_ring) / (tau_end + 1), double(tr_bar) / (tau_end + 1));
+    const long long tr_loop = clock64() - tr_l0;
+    if (lane == 0 && (G == 1 || (G >= 4 && G <= 8)) && residuals && ISMG_CL_TRACE_WARPS)
+        printf("TRACE G=%d steps=%d warp=%2d loop=%lld int=%lld bar=%lld\n", G, tau_end + 1, warp, tr_loop, tr_int,
+               tr_bar);
 #endif
 }
 
 template <int Kind, int BM>
-__global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom T, const double* spec_g,
+__global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGeom T, const double* spec_g,
                                                                double* backup) {
     __shared__ ClShared cs;
     Ctl* st = P.ctl;
@@ -467,7 +392,7 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
             const int jj = k / T.ncx, I = k - jj * T.ncx;
             bsm[jj * T.bpitch + I] = P.cb.at(I, B.J0 + jj);
         }
-    const int spec_words = 10 * T.ncls + (T.ring + 1) / 2;
+    const int spec_words = 10 * (T.ncls + 1) + (T.ring + 1) / 2;
     for (int k = threadIdx.x; k < spec_words; k += blockDim.x) spec[k] = spec_g[k];
     cluster.sync();
     double* my_backup = backup + size_t(B.c) * nxs;
@@ -481,14 +406,20 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
         if (G > 1)
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) my_backup[k] = B.xs[k];  // checkpoint
         const long long tg0 = gtimer();
+#ifdef ISMG_CL_TRACE
+        const long long ck0 = clock64();
+#endif
         cl_group<Kind, BM>(T, B, P.cb, cs, G, true);
         gns += gtimer() - tg0;
+#ifdef ISMG_CL_TRACE
+        if (threadIdx.x == 0 && B.c == 0) printf("GROUP G=%d ns=%lld cycles=%lld\n", G, gtimer() - tg0, clock64() - ck0);
+#endif
         steps += dmax + kLag * (G - 1) + 5;
         // cluster-wide first sweep whose residual passes tol_coarse
         {
             const int nrb = (B.J1 - B.J0 + 31) >> 5;
             for (int g = threadIdx.x; g < G; g += blockDim.x) {
-                double m = fmax(cs.cmax[0][g], __longlong_as_double((long long)cs.rmax[g]));
+                double m = cs.cmax[0][g];
                 for (int r = 1; r < nrb; ++r) m = fmax(m, cs.cmax[r][g]);
                 cs.gmax[g] = m;
             }
@@ -519,6 +450,9 @@ __global__ void __launch_bounds__(kClThreads) coarse_cl_kernel(Params P, ClGeom 
             const long long tg0 = gtimer();
             cl_group<Kind, BM>(T, B, P.cb, cs, first + 1, false);
             gns += gtimer() - tg0;
+#ifdef ISMG_CL_TRACE
+            if (threadIdx.x == 0 && B.c == 0) printf("REPLAY G=%d ns=%lld\n", first + 1, gtimer() - tg0);
+#endif
             steps += dmax + kLag * first + 1;
             done += first + 1;
             break;
@@ -622,14 +556,6 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     if (T.stdw[0] == 0.0) return false;
     static const double ismg[9] = {-3.0, 0.5, 0.5, 0.5, 0.5, 0.25, 0.25, 0.25, 0.25};
     static const double five[9] = {-4.0, 1.0, 1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
-    T.kind = 0;
-    bool is_ismg = !op.five_point, is_five = op.five_point;
-    for (int sl = 0; sl < 9; ++sl) {
-        is_ismg = is_ismg && same_bits(T.stdw[sl], ismg[sl]);
-        is_five = is_five && (sl >= 5 || same_bits(T.stdw[sl], five[sl]));
-    }
-    if (is_ismg) T.kind = 1;
-    if (is_five) T.kind = 2;
     std::vector<std::array<double, 9>> cls;
     std::vector<int> ring_cls(size_t(T.ring), 0);
     auto classify = [&](int r, int I, int J) {
@@ -648,11 +574,13 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     for (int J = 0; J < op.ncy; ++J) classify(2 * op.ncx + J, 0, J), classify(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
     T.ncls = int(cls.size());
     if (T.ncls > 1024) return false;
-    T.fastdiv = 1;  // Markstein's correction per class divisor, spot-checked
+    T.fastdiv = 1;  // Markstein's correction per divisor (ring classes and the interior), spot-checked
+    T.stdy = 1.0 / T.stdw[0];
     uint64_t st = 0x9E3779B97F4A7C15ull;
-    for (const auto& w : cls) {
-        if (w[0] == 0.0) return false;  // singular ring row: the op-level path raises
-        const double b = w[0], y = 1.0 / b;
+    for (size_t c = 0; c <= cls.size(); ++c) {
+        const double b = c < cls.size() ? cls[c][0] : T.stdw[0];
+        if (b == 0.0) return false;  // singular ring row: the op-level path raises
+        const double y = 1.0 / b;
         for (int k = 0; k < 20000 && T.fastdiv; ++k) {
             st ^= st << 13, st ^= st >> 7, st ^= st << 17;
             const double a = std::ldexp(double(st >> 11) * 0x1.0p-53 + 0.5, int((st >> 3) % 120) - 60) *
@@ -661,12 +589,33 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
             if (!same_bits(mk, a / b)) T.fastdiv = 0;
         }
     }
-    spec.assign(size_t(10) * T.ncls + size_t(T.ring + 1) / 2, 0.0);
-    for (int c = 0; c < T.ncls; ++c) {
-        for (int sl = 0; sl < 9; ++sl) spec[size_t(10) * c + sl] = cls[size_t(c)][size_t(sl)];
-        spec[size_t(10) * c + 9] = 1.0 / cls[size_t(c)][0];
+    // zero weights facing only ghosts (+0.0) need no skip (see term()); corners
+    // of a five-point operator are never read
+    static const int dx[9] = {0, 1, -1, 0, 0, 1, -1, 1, -1}, dy[9] = {0, 0, 0, 1, -1, 1, 1, -1, -1};
+    const int nsl = T.five ? 5 : 9;
+    bool zghost = true;
+    for (int sl = 1; sl < nsl; ++sl) zghost = zghost && T.stdw[sl] != 0.0;
+    for (int r = 0; r < T.ring && zghost; ++r) {
+        int I, J;
+        if (r < op.ncx) I = r, J = 0;
+        else if (r < 2 * op.ncx) I = r - op.ncx, J = op.ncy - 1;
+        else if (r < 2 * op.ncx + op.ncy) I = 0, J = r - 2 * op.ncx;
+        else I = op.ncx - 1, J = r - 2 * op.ncx - op.ncy;
+        for (int sl = 1; sl < nsl; ++sl) {
+            const int In = I + dx[sl], Jn = J + dy[sl];
+            const bool ghost = In < 0 || In >= op.ncx || Jn < 0 || Jn >= op.ncy;
+            if (cls[size_t(ring_cls[size_t(r)])][size_t(sl)] == 0.0 && !ghost) zghost = false;
+        }
     }
-    std::memcpy(spec.data() + size_t(10) * T.ncls, ring_cls.data(), sizeof(int) * ring_cls.size());
+    T.kind = (T.five ? 1 : 0) | (zghost ? 0 : 2);
+    // table: classes 0..ncls-1 (ring), class ncls (interior), then the ring's class ids
+    spec.assign(size_t(10) * (T.ncls + 1) + size_t(T.ring + 1) / 2, 0.0);
+    for (int c = 0; c <= T.ncls; ++c) {
+        const double* w = c < T.ncls ? cls[size_t(c)].data() : T.stdw;
+        for (int sl = 0; sl < 9; ++sl) spec[size_t(10) * c + sl] = w[sl];
+        spec[size_t(10) * c + 9] = 1.0 / w[0];
+    }
+    std::memcpy(spec.data() + size_t(10) * (T.ncls + 1), ring_cls.data(), sizeof(int) * ring_cls.size());
     // pitches = 3 (mod 16) doubles (conflict-free wavefront lanes), >= ncx + 2
     T.pitch = (op.ncx + 2) + ((3 - (op.ncx + 2) % 16) + 16) % 16;
     T.bpitch = op.ncx + ((3 - op.ncx % 16) + 16) % 16;
@@ -697,27 +646,27 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
 
 size_t cl_backup_doubles(const ClGeom& T) { return size_t(T.csize) * size_t(T.band + 2) * T.pitch; }
 
+template <int Kind>
+void launch_kind(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem, cudaStream_t st) {
+    if (T.bsmem == 2) launch_one<Kind, 2>(P, T, spec, backup, smem, st);
+    else if (T.bsmem == 1) launch_one<Kind, 1>(P, T, spec, backup, smem, st);
+    else launch_one<Kind, 0>(P, T, spec, backup, smem, st);
+}
 void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
                       cudaStream_t st) {
-    const int k = T.kind, m = T.bsmem;
-    if (k == 1) {
-        if (m == 2) launch_one<1, 2>(P, T, spec, backup, smem, st);
-        else if (m == 1) launch_one<1, 1>(P, T, spec, backup, smem, st);
-        else launch_one<1, 0>(P, T, spec, backup, smem, st);
-    } else if (k == 2) {
-        if (m == 2) launch_one<2, 2>(P, T, spec, backup, smem, st);
-        else if (m == 1) launch_one<2, 1>(P, T, spec, backup, smem, st);
-        else launch_one<2, 0>(P, T, spec, backup, smem, st);
-    } else {
-        if (m == 2) launch_one<0, 2>(P, T, spec, backup, smem, st);
-        else if (m == 1) launch_one<0, 1>(P, T, spec, backup, smem, st);
-        else launch_one<0, 0>(P, T, spec, backup, smem, st);
+    switch (T.kind) {
+        case 0: launch_kind<0>(P, T, spec, backup, smem, st); break;
+        case 1: launch_kind<1>(P, T, spec, backup, smem, st); break;
+        case 2: launch_kind<2>(P, T, spec, backup, smem, st); break;
+        default: launch_kind<3>(P, T, spec, backup, smem, st); break;
     }
 }
+template <int Kind>
+void set_attrs_kind(size_t bytes) {
+    set_attrs<Kind, 0>(bytes), set_attrs<Kind, 1>(bytes), set_attrs<Kind, 2>(bytes);
+}
 void set_coarse_cl_smem(size_t bytes) {
-    set_attrs<0, 0>(bytes), set_attrs<1, 0>(bytes), set_attrs<2, 0>(bytes);
-    set_attrs<0, 1>(bytes), set_attrs<1, 1>(bytes), set_attrs<2, 1>(bytes);
-    set_attrs<0, 2>(bytes), set_attrs<1, 2>(bytes), set_attrs<2, 2>(bytes);
+    set_attrs_kind<0>(bytes), set_attrs_kind<1>(bytes), set_attrs_kind<2>(bytes), set_attrs_kind<3>(bytes);
 }
 
 }  // namespace fz

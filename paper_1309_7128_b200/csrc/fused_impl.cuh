@@ -299,7 +299,8 @@ struct ClGeom {
     int bsmem;          // rhs: 1 shared memory, 2 Tensor Memory, 0 read through L1
     int ring, ncls, fastdiv, kind;
     bool five;
-    double stdw[9];
+    double stdw[9];  // interior weights (slot order C, E, W, N, S, NE, NW, SE, SW)
+    double stdy;     // RN(1 / stdw[0]): Markstein's reciprocal (fastdiv)
 };
 bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem);
 size_t cl_backup_doubles(const ClGeom& T);
