@@ -240,77 +240,86 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
 #ifdef ISMG_CL_TRACE
         const long long c0 = clock64();
 #endif
-        if (w_on) {
-            const int bu0 = tau, br0 = residuals ? tau - 4 : -1;
-            int gu = 0, guh = -1, gr = 0, grh = -1;
-            if (bu0 >= dlo) {
-                const int g_lo = max(0, (bu0 - dhi + kLag - 1) >> 3);
-                guh = min(G - 1, (bu0 - dlo) >> 3);
-                gu = g_lo + ((h - g_lo) & (kH - 1));
-            }
-            if (br0 >= dlo) {
-                const int g_lo = max(0, (br0 - dhi + kLag - 1) >> 3);
-                grh = min(G - 1, (br0 - dlo) >> 3);
-                gr = g_lo + ((h - g_lo) & (kH - 1));
-            }
-            const int Iu0 = bu0 - 2 * J, Ir0 = br0 - 2 * J;
-#pragma unroll 1
-            while (gu <= guh || gr <= grh) {
-                const bool du = gu <= guh, dres = gr <= grh;
-                const int Iu = Iu0 - kLag * gu, Ir = Ir0 - kLag * gr;
-                const bool oku = du && rowin && unsigned(Iu) < ncx;
-                const bool okr = dres && rowin && unsigned(Ir) < ncx;
-                const int Iuc = oku ? Iu : 0, Irc = okr ? Ir : 0;  // clamped: every lane reads a valid cell
-                // weights of the two cells: interior, first / last column, or (first /
-                // last row) by column from the ring's class ids
-                const int offu = ringrow ? B.so + 10 * ring_cls[rbase + Iuc]
-                                         : (Iu == 0 ? off_w : Iu == T.ncx - 1 ? off_e : off_i);
-                const int offr = ringrow ? B.so + 10 * ring_cls[rbase + Irc]
-                                         : (Ir == 0 ? off_w : Ir == T.ncx - 1 ? off_e : off_i);
-                Wts Wu, Wr;
-                load_wts(offu, Wu);
-                load_wts(offr, Wr);
-                double bu, br_;
+        // one update (diagonal dU) and one residual (diagonal dR, sweep gr) per lane
+        auto pair = [&](bool du, bool dres, int dU, int dR, int gr) {
+            const int Iu = dU - 2 * J, Ir = dR - 2 * J;
+            const bool oku = du && rowin && unsigned(Iu) < ncx;
+            const bool okr = dres && rowin && unsigned(Ir) < ncx;
+            const int Iuc = oku ? Iu : 0, Irc = okr ? Ir : 0;  // clamped: every lane reads a valid cell
+            // weights of the two cells: interior, first / last column, or (first /
+            // last row) by column from the ring's class ids
+            const int offu = ringrow ? B.so + 10 * ring_cls[rbase + Iuc]
+                                     : (Iu == 0 ? off_w : Iu == T.ncx - 1 ? off_e : off_i);
+            const int offr = ringrow ? B.so + 10 * ring_cls[rbase + Irc]
+                                     : (Ir == 0 ? off_w : Ir == T.ncx - 1 ? off_e : off_i);
+            Wts Wu, Wr;
+            load_wts(offu, Wu);
+            load_wts(offr, Wr);
+            double bu, br_;
 #ifdef X_NOTMEM
-                if (true) { bu = 0.1; br_ = 0.2; } else
+            if (true) { bu = 0.1; br_ = 0.2; } else
 #endif
-                if constexpr (BM == 2) {  // rhs of the cells on diagonals d: TMEM column (d mod 256), warp-uniform
-                    uint32_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
-                    if (du) tm_ld2(tq + 2u * uint32_t((bu0 - kLag * gu) & 255), lo0, hi0);
-                    if (dres) tm_ld2(tq + 2u * uint32_t((br0 - kLag * gr) & 255), lo1, hi1);
-                    tm_wait_ld();
-                    bu = __hiloint2double(int(hi0), int(lo0));
-                    br_ = __hiloint2double(int(hi1), int(lo1));
-                } else if constexpr (BM == 1) {
-                    bu = cl_dyn[browo + Iuc];
-                    br_ = cl_dyn[browo + Irc];
-                } else {
-                    bu = __ldg(brow + Iuc);
-                    br_ = __ldg(brow + Irc);
-                }
-                // both cells, branch-free, so their independent fp64 chains interleave
-                const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
-                const Nbr vu = gather(rowo + Iuc, pitch, false, kFive);
-                const double rres = apply_lane<true, kFive, kSel>(Wr, vr, br_, fastdiv);
-                const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
-                if (oku) {  // update of sweep gu
-                    cl_dyn[rowo + Iu] = out;
+            if constexpr (BM == 2) {  // rhs of the cells on diagonals d: TMEM column (d mod 256), warp-uniform
+                uint32_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+                if (du) tm_ld2(tq + 2u * uint32_t(dU & 255), lo0, hi0);
+                if (dres) tm_ld2(tq + 2u * uint32_t(dR & 255), lo1, hi1);
+                tm_wait_ld();
+                bu = __hiloint2double(int(hi0), int(lo0));
+                br_ = __hiloint2double(int(hi1), int(lo1));
+            } else if constexpr (BM == 1) {
+                bu = cl_dyn[browo + Iuc];
+                br_ = cl_dyn[browo + Irc];
+            } else {
+                bu = __ldg(brow + Iuc);
+                br_ = __ldg(brow + Irc);
+            }
+            // both cells, branch-free, so their independent fp64 chains interleave
+            const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
+            const Nbr vu = gather(rowo + Iuc, pitch, false, kFive);
+            const double rres = apply_lane<true, kFive, kSel>(Wr, vr, br_, fastdiv);
+            const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
+            if (oku) {  // update of sweep gu
+                cl_dyn[rowo + Iu] = out;
 #ifndef X_NOMIRROR
-                    if (mirror_s) B.south[Iu] = out;
-                    if (mirror_n) B.north[Iu] = out;
+                if (mirror_s) B.south[Iu] = out;
+                if (mirror_n) B.north[Iu] = out;
 #endif
+            }
+            if (dres) {  // residual of sweep gr (inputs final since step tau - 1)
+                double m = okr ? fabs(rres) : 0.0;
+                m = (m != m) ? 0.0 : m;  // std::max drops NaN
+                if (one_g) {  // the warp's only sweep: keep a per-lane max, fold once per group
+                    lmax = fmax(lmax, m);
+                } else {
+                    m = warp_max_nonneg(m);
+                    if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
                 }
-                if (dres) {  // residual of sweep gr (inputs final since step tau - 1)
-                    double m = okr ? fabs(rres) : 0.0;
-                    m = (m != m) ? 0.0 : m;  // std::max drops NaN
-                    if (one_g) {  // the warp's only sweep: keep a per-lane max, fold once per group
-                        lmax = fmax(lmax, m);
-                    } else {
-                        m = warp_max_nonneg(m);
-                        if (lane == 0) cs.cmax[rb][gr] = fmax(cs.cmax[rb][gr], m);  // (rb, gr): this warp alone
-                    }
+            }
+        };
+        if (w_on) {
+            if (one_g) {  // this warp's only sweep is g = h
+                const int dU = tau - kLag * h, dR = dU - 4;
+                const bool du = h < G && dU >= dlo && dU <= dhi;
+                const bool dres = residuals && h < G && dR >= dlo && dR <= dhi;
+                if (du || dres) pair(du, dres, dU, dR, h);
+            } else {
+                const int bu0 = tau, br0 = residuals ? tau - 4 : -1;
+                int gu = 0, guh = -1, gr = 0, grh = -1;
+                if (bu0 >= dlo) {
+                    const int g_lo = max(0, (bu0 - dhi + kLag - 1) >> 3);
+                    guh = min(G - 1, (bu0 - dlo) >> 3);
+                    gu = g_lo + ((h - g_lo) & (kH - 1));
                 }
-                gu += kH, gr += kH;
+                if (br0 >= dlo) {
+                    const int g_lo = max(0, (br0 - dhi + kLag - 1) >> 3);
+                    grh = min(G - 1, (br0 - dlo) >> 3);
+                    gr = g_lo + ((h - g_lo) & (kH - 1));
+                }
+#pragma unroll 1
+                while (gu <= guh || gr <= grh) {
+                    pair(gu <= guh, gr <= grh, bu0 - kLag * gu, br0 - kLag * gr, gr);
+                    gu += kH, gr += kH;
+                }
             }
         }
 #ifdef ISMG_CL_TRACE

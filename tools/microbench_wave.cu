@@ -43,6 +43,28 @@ __global__ void wave(double* out, long long* cyc, int steps, int act) {
                 ra += 0.25 * rne; ra += 0.25 * rnw; ra += 0.25 * rse; ra += 0.25 * rsw;
                 xs[rowo + Iu] = div_m3(0.1 - acc);
                 lmax = fmax(lmax, fabs(0.1 - ra));
+            } else if (MODE == 2 || MODE == 3) {  // pair with per-lane weights from shared memory
+                int off = 129 * P + 1;  // class table row (10 doubles, 16-byte aligned)
+                if (MODE == 3 && lane == 0) off += 10 * (int(xs[128 * P + (Iu & 7)]) & 1);
+                const double2* wp = reinterpret_cast<const double2*>(xs + off);
+                const double2 w01 = wp[0], w23 = wp[1], w45 = wp[2], w67 = wp[3], w89 = wp[4];
+                const double e = pu[1], w = pu[-1], n = pu[P], s = pu[-P], ne = pu[P + 1], nw = pu[P - 1],
+                             se = pu[1 - P], sw = pu[-1 - P];
+                const double rc = pr[0], re = pr[1], rw = pr[-1], rn = pr[P], rs = pr[-P], rne = pr[P + 1],
+                             rnw = pr[P - 1], rse = pr[1 - P], rsw = pr[-1 - P];
+                const double2* wq = reinterpret_cast<const double2*>(xs + off + 20);
+                const double2 v01 = wq[0], v23 = wq[1], v45 = wq[2], v67 = wq[3], v89 = wq[4];
+                double acc = 0.0;
+                acc += w01.y * e; acc += w23.x * w; acc += w23.y * n; acc += w45.x * s;
+                acc += w45.y * ne; acc += w67.x * nw; acc += w67.y * se; acc += w89.x * sw;
+                double ra = v01.x * rc;
+                ra += v01.y * re; ra += v23.x * rw; ra += v23.y * rn; ra += v45.x * rs;
+                ra += v45.y * rne; ra += v67.x * rnw; ra += v67.y * rse; ra += v89.x * rsw;
+                const double num = 0.1 - acc;
+                const double q = __dmul_rn(num, w89.y);
+                const double r = __fma_rn(-q, w01.x, num);
+                xs[rowo + Iu] = __fma_rn(r, w89.y, q);
+                lmax = fmax(lmax, fabs(0.1 - ra));
             } else {  // update only
                 const double e = pu[1], w = pu[-1], n = pu[P], s = pu[-P], ne = pu[P + 1], nw = pu[P - 1],
                              se = pu[1 - P], sw = pu[-1 - P];
@@ -74,7 +96,9 @@ int main() {
     const size_t smem = 130 * P * sizeof(double);
     cudaFuncSetAttribute(wave<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(wave<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    for (int threads : {512, 768}) {
+    cudaFuncSetAttribute(wave<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(wave<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    for (int threads : {512}) {
         barrier_only<<<1, threads>>>(cyc, steps);
         cudaDeviceSynchronize();
         printf("threads %d barrier only: %.1f cycles/step\n", threads, double(cyc[0]) / steps);
@@ -84,8 +108,14 @@ int main() {
             const double c0 = double(cyc[0]) / steps;
             wave<1><<<1, threads, smem>>>(out, cyc, steps, act);
             cudaDeviceSynchronize();
-            printf("threads %d active warps %2d: pair %.1f  update-only %.1f cycles/step\n", threads, act, c0,
-                   double(cyc[0]) / steps);
+            const double c1 = double(cyc[0]) / steps;
+            wave<2><<<1, threads, smem>>>(out, cyc, steps, act);
+            cudaDeviceSynchronize();
+            const double c2 = double(cyc[0]) / steps;
+            wave<3><<<1, threads, smem>>>(out, cyc, steps, act);
+            cudaDeviceSynchronize();
+            printf("threads %d active warps %2d: pair %.1f  update-only %.1f  smem-weights %.1f  +class %.1f\n", threads,
+                   act, c0, c1, c2, double(cyc[0]) / steps);
         }
     }
     return 0;
