@@ -27,6 +27,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include <cooperative_groups.h>
@@ -630,26 +631,30 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     T.bpitch = op.ncx + ((3 - op.ncx % 16) + 16) % 16;
     const size_t cap = 200 * 1024;
     const size_t spec_bytes = spec.size() * sizeof(double);
-    // smallest cluster whose bands fit shared memory (a cluster barrier costs ~6x a
-    // CTA barrier); rhs in shared memory if it fits too, else in Tensor Memory
-    // (bands <= 128 rows, ncx <= 256), else read through L1
-    for (int C = 1; C <= 16; C *= 2)
+    // Band height: 32 rows per CTA when the cluster allows it. One 32-row band per
+    // SM spreads a step's cells over C SMs; the cluster barrier per step (~600
+    // cycles against ~50 for a CTA barrier) is repaid from about 5 sweeps in
+    // flight up (measured at 128^2: 252 ms of coarse groups at C = 4 against 346 at
+    // C = 1 over a 4096^2 step). rhs in shared memory if it fits, else in Tensor
+    // Memory (bands <= 128 rows, ncx <= 256), else read through L1.
+    int rmin = 32;  // tuning hook: ISMG_CL_BAND = smallest band height tried
+    if (const char* e = getenv("ISMG_CL_BAND")) rmin = std::max(32, atoi(e) / 32 * 32);
+    for (int R = rmin; R <= 32 * kMaxRowBlocks; R *= 2) {
+        const int C = (op.ncy + R - 1) / R;
+        if (C > 16) continue;
         for (int bm : {1, 2, 0}) {
-            int R = (op.ncy + C - 1) / C;
-            R = (R + 31) / 32 * 32;  // whole 32-row blocks
-            if (R > 32 * kMaxRowBlocks) continue;
-            if ((op.ncy + R - 1) / R < C) continue;  // no empty CTAs
             if (bm == 2 && (R > 128 || op.ncx > 256)) continue;
             const size_t bytes = (size_t(R + 2) * T.pitch + (bm == 1 ? size_t(R) * T.bpitch : 0)) * sizeof(double) +
                                  spec_bytes;
             if (bytes <= cap) {
-                T.csize = (op.ncy + R - 1) / R;
+                T.csize = C;
                 T.band = R;
                 T.bsmem = bm;
                 smem = bytes;
                 return true;
             }
         }
+    }
     return false;
 }
 
