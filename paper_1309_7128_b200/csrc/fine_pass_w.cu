@@ -29,8 +29,15 @@ namespace fz {
 
 namespace {
 
+// Minimum resident CTAs (= warps) per SM requested from ptxas, i.e. its register
+// cap. 14 caps the single-GPU kernel at 128 registers without spills and runs
+// 14 warps per SM instead of 12: 133 against 152 us per 4096^2 pass
+// (tools/probe_fine.py; 12: 152, 13: 148, 15: 133, 16: 137, 20: 196 with spills).
 #ifndef ISMG_FINE_MINB
-#define ISMG_FINE_MINB 1  // minimum resident CTAs per SM requested from ptxas (register cap)
+#define ISMG_FINE_MINB 14
+#endif
+#ifndef ISMG_FINE_MINB_MP
+#define ISMG_FINE_MINB_MP 1  // the multi-GPU variant spills at 14
 #endif
 
 constexpr int kRowW = 128;  // ring row: columns [a-4, a+124)
@@ -503,7 +510,7 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
 }
 
 template <bool MP>
-__global__ void __launch_bounds__(32, ISMG_FINE_MINB) fine_pass_w_kernel(Params P, int nq) {
+__global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : ISMG_FINE_MINB) fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
     if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
