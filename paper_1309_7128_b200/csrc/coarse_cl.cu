@@ -257,9 +257,6 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
             load_wts(offu, Wu);
             load_wts(offr, Wr);
             double bu, br_;
-#ifdef X_NOTMEM
-            if (true) { bu = 0.1; br_ = 0.2; } else
-#endif
             if constexpr (BM == 2) {  // rhs of the cells on diagonals d: TMEM column (d mod 256), warp-uniform
                 uint32_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
                 if (du) tm_ld2(tq + 2u * uint32_t(dU & 255), lo0, hi0);
@@ -281,10 +278,8 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
             const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
             if (oku) {  // update of sweep gu
                 cl_dyn[rowo + Iu] = out;
-#ifndef X_NOMIRROR
                 if (mirror_s) B.south[Iu] = out;
                 if (mirror_n) B.north[Iu] = out;
-#endif
             }
             if (dres) {  // residual of sweep gr (inputs final since step tau - 1)
                 double m = okr ? fabs(rres) : 0.0;

@@ -41,7 +41,10 @@ namespace {
 #endif
 
 constexpr int kRowW = 128;  // ring row: columns [a-4, a+124)
-constexpr int kRingW = 6;   // rows in flight
+#ifndef ISMG_FINE_RING
+#define ISMG_FINE_RING 6
+#endif
+constexpr int kRingW = ISMG_FINE_RING;  // rows in flight
 
 struct SmemW {
     double x[kRingW][kRowW];
