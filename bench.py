@@ -329,8 +329,9 @@ def run_ours(args, rank, world, local_rank):
             "data": "synthetic (quiescent lid-driven cavity, seed 0)",
             "config": {"workload": "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (config 2)" % (n, n),
                        "global_batch": 1, "seq_len": 0,
-                       "parallelism": ("y-strips x%d (NCCL halo/partials/coarse-rhs allgather per fine pass; "
-                                       "coarse solve replicated)" % world) if dist else "single GPU",
+                       "parallelism": ("y-strips x%d (halo rows pushed over NVLink by the fine pass, partials "
+                                       "and coarse-rhs rows pulled from peer memory; coarse solve replicated)"
+                                       % world) if dist else "single GPU",
                        "steps_timed": "projection steps 1..%d" % args.steps,
                        "l2": "inputs larger than L2 (x, scratch, b: 3 x 134 MB vs 126 MB L2)",
                        "fine_sweeps": int(fine_all), "coarse_sweeps": int(coarse)},

@@ -345,30 +345,74 @@ void launch_finalize(const Params& P, View xuser, cudaStream_t st) {
 // ranks' coarse rows, and apply the reference's branch logic. The next pass
 // reads its halo rows straight from the gathered packs.
 __global__ void mp_unpack_kernel(Params P) {
-    const double* g = P.gathered;
+    __shared__ int s_pass;
+    Ctl* st = P.ctl;
+#ifdef ISMG_MP_TRACE
+    const long long tu0 = gtimer();
+#endif
+    const unsigned long long want = st->mp_seq + 1ull;  // flag value of this slot's pass
+    if (threadIdx.x == 0) {
+        const volatile unsigned long long* f = P.xflag[P.rank];
+        int pass = f[P.rank] >= want;  // a fine pass ran in this slot (on every rank alike)
+        if (pass) {
+            const long long t0 = gtimer();
+            for (int q = 0; q < P.nranks && pass; ++q)
+                while (f[q] < want)
+                    if (gtimer() - t0 > 4000000000ll) {  // a peer is gone: stop instead of hanging
+                        st->mp_error = 1, st->phase = kDone, pass = 0;
+                        break;
+                    }
+            __threadfence_system();
+        }
+        s_pass = pass;
+    }
+    __syncthreads();
+    if (!s_pass) return;
     const int L = P.pack_len;
-    // coarse rhs rows of every rank -> cb (used by the next coarse visit)
+    const int64_t po = int64_t((want - 1ull) & 1ull) * P.nranks * L;  // this pass's parity
+    // coarse rhs rows of every rank -> cb (used by the next coarse visit), pulled
+    // from each rank's own slot (peer memory over NVLink)
     for (int r = 0; r < P.nranks; ++r) {
         int f0, f1;
         strip_of(P.ny, P.tile, P.nranks, r, &f0, &f1);
         const int c0 = f0 / P.tile, c1 = (f1 + P.tile - 1) / P.tile;
-        const double* src = g + int64_t(r) * L + 8;
-        for (int k = threadIdx.x; k < (c1 - c0) * P.ncx; k += blockDim.x) {
-            const int jj = k / P.ncx, I = k - jj * P.ncx;
-            P.cb.at(I, c0 + jj) = src[int64_t(jj) * P.cb.pitch + I];
+        const double* src = P.xch[r] + po + int64_t(r) * L + 8;
+        const int n = (c1 - c0) * P.ncx;
+        for (int k0 = threadIdx.x; k0 < n; k0 += 4 * blockDim.x) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // four loads in flight per thread
+                const int k = k0 + u * int(blockDim.x);
+                const int jj = k / P.ncx, I = k - jj * P.ncx;
+                v[u] = k < n ? __ldcv(src + int64_t(jj) * P.cb.pitch + I) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + u * int(blockDim.x);
+                const int jj = k / P.ncx, I = k - jj * P.ncx;
+                if (k < n) P.cb.at(I, c0 + jj) = v[u];
+            }
         }
     }
-    if (threadIdx.x == 0 && g[2] != 0.0) {  // a fine pass ran in this slot (all ranks alike)
+    if (threadIdx.x == 0) {  // pass partials reduced in rank order: identical bits on every rank
         double m = 0.0, c = 0.0, sx = 0.0;
         for (int r = 0; r < P.nranks; ++r) {
-            const double* v = g + int64_t(r) * L;
-            m = fmax(m, v[0]);
-            c = fmax(c, v[1]);
-            sx += v[4];
+            const double* v = P.xch[r] + po + int64_t(r) * L;
+            m = fmax(m, __ldcv(v + 0));
+            c = fmax(c, __ldcv(v + 1));
+            sx += __ldcv(v + 4);
         }
-        fine_decide(P, int(g[3]), m, sx, c);
+        const double* g = P.xch[0] + po;
+        st->mp_seq = want;
+        fine_decide(P, int(__ldcv(g + 3)), m, sx, c);
+#ifdef ISMG_MP_TRACE
+        const long long tu1 = gtimer();
+        if (want % 64 == 0)
+            printf("MPTRACE rank %d seq %llu fine %lld gap %lld unpack %lld\n", P.rank, want,
+                   (long long)(st->mp_t1 - st->mp_t0), (long long)(tu0 - (long long)st->mp_t1), tu1 - tu0);
+        st->mp_t0 = ~0ull;
+#endif
     }
-    if (threadIdx.x == 0) P.rank_part[2] = 0.0;  // this rank's pass flag, for the next slot
 }
 void launch_mp_unpack(const Params& P, cudaStream_t st) { mp_unpack_kernel<<<1, 1024, 0, st>>>(P); }
 

@@ -36,6 +36,9 @@ namespace {
 #ifndef ISMG_FINE_MINB
 #define ISMG_FINE_MINB 14
 #endif
+#ifndef ISMG_MP_FENCE_SC
+#define ISMG_MP_FENCE_SC 0
+#endif
 #ifndef ISMG_FINE_MINB_MP
 #define ISMG_FINE_MINB_MP 1  // the multi-GPU variant spills at 14
 #endif
@@ -118,43 +121,62 @@ struct Geo {
     double c, fwS, fwN;
     double* outp;
     int64_t pitch;
-    // multi-GPU: rows [hj0, hj0+3) also go to hs0, rows [hj1, hj1+3) to hs1 (nullptr: none)
-    double* hs0;
-    double* hs1;
-    int hj0, hj1;
 };
 
-__device__ __forceinline__ void halo_geo(Geo& G, const Params& P, int c0) {
-    G.hs0 = G.hs1 = nullptr;
-    G.hj0 = G.hj1 = -1000;
-    if (!P.mp) return;
-    if (P.row0 > 0) G.hs0 = P.halo_send[0] + kXOff + c0, G.hj0 = P.row0;
-    if (P.row1 < P.ny) G.hs1 = P.halo_send[1] + kXOff + c0, G.hj1 = P.row1 - 3;
+// release fence at system scope: orders this thread's peer stores before its
+// later ticket / flag writes (no sequential-consistency fence needed)
+__device__ __forceinline__ void fence_release_sys() {
+#if ISMG_MP_FENCE_SC
+    __threadfence_system();
+#else
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
 }
 
-// store a finished quad row j (multi-GPU: and its halo copy for the neighbour rank)
-template <bool MP>
+// this rank's own pack slot of pass parity p in its exchange buffer
+__device__ __forceinline__ double* my_pack(const Params& P, int p) {
+    return P.xch[P.rank] + (int64_t(p) * P.nranks + P.rank) * P.pack_len;
+}
+
+
+// Multi-GPU, end of a CTA's pass: the boundary rows it relaxed (read back from
+// x: the output of a sweep / prolongation, the unchanged input of a residual
+// pass) go into this rank's pack slot of parity p on every rank, over NVLink for
+// the peers, followed by a system-scope release fence. Only the CTAs holding
+// the strip's first / last 3 rows push; tile sums and partials stay in the
+// local slot, where mp_unpack_kernel on every rank pulls them from.
+__device__ __forceinline__ void mp_push(const Params& P, const Lane& L, const Geo& G, int p, const double* xrows) {
+    const int64_t o0 = (int64_t(p) * P.nranks + P.rank) * P.pack_len;
+    bool pushed = false;
+    for (int h = 0; h < 2; ++h) {
+        if (h == 0 ? P.row0 == 0 : P.row1 == P.ny) continue;
+        const int hj = h == 0 ? P.row0 : P.row1 - 3;
+        for (int j = max(hj, G.r0); j < min(hj + 3, G.r1); ++j) {
+            pushed = true;
+            if (!L.owned) continue;
+            const double* src = xrows + int64_t(j) * P.pitch;
+            const double2 v01 = *reinterpret_cast<const double2*>(src);
+            const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
+            const int64_t off = o0 + P.h_off[h] + int64_t(j - hj) * P.pitch + kXOff + L.c0;
+            for (int q = 0; q < P.nranks; ++q) {
+                reinterpret_cast<double2*>(P.xch[q] + off)[0] = v01;
+                reinterpret_cast<double2*>(P.xch[q] + off)[1] = v23;
+            }
+        }
+    }
+    if (pushed) fence_release_sys();
+}
+
+// store a finished quad row j
 __device__ __forceinline__ void put_row(const Geo& G, const Lane& L, int j, const double* v) {
     double* dst = G.outp + int64_t(j) * G.pitch;
-    double* hs = nullptr;
-    if constexpr (MP) {
-        if (unsigned(j - G.hj0) < 3u) hs = G.hs0 + int64_t(j - G.hj0) * G.pitch;
-        if (unsigned(j - G.hj1) < 3u) hs = G.hs1 + int64_t(j - G.hj1) * G.pitch;
-    }
     if (!L.spec) {
         reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
         reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
-        if (MP && hs) {
-            reinterpret_cast<double2*>(hs)[0] = make_double2(v[0], v[1]);
-            reinterpret_cast<double2*>(hs)[1] = make_double2(v[2], v[3]);
-        }
     } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (L.dom[q]) {
-                dst[q] = v[q];
-                if (MP && hs) hs[q] = v[q];
-            }
+            if (L.dom[q]) dst[q] = v[q];
     }
 }
 
@@ -260,7 +282,7 @@ __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L,
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));  // std::max(rmax, |r|): NaN dropped
             A.sx = A.sx + ((x3[0] + x3[1]) + (x3[2] + x3[3]));   // out-of-domain cells hold 0
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            put_row<MP>(G, L, j, x3);
+            put_row(G, L, j, x3);
         }
     }
     // row k takes the slot of row k-4
@@ -270,12 +292,14 @@ __device__ __forceinline__ void step_w(const SmemW& sm, int slot, const Lane& L,
 
 // tile row-block complete: fold the g = tile/4 lanes of every coarse cell
 // (groups start at lane 1; the tile is a power of two)
-__device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int j, int lg, Acc& A) {
+template <bool MP>
+__device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int j, int lg, Acc& A, double* mpk) {
     const int g = P.tile >> 2;
     double v = A.tacc;
     for (int o = g >> 1; o > 0; o >>= 1) v = v + __shfl_down_sync(kFull, v, o);
     if (L.owned && ((L.l - 1) & (g - 1)) == 0 && L.dom[0]) {
-        P.cbw.at(L.c0 >> lg, j >> lg) = v;
+        if (MP) mpk[P.cb_off + int64_t(j >> lg) * P.cb_pitch + (L.c0 >> lg)] = v;  // multi-GPU: own pack slot
+        else P.cbw.at(L.c0 >> lg, j >> lg) = v;
         A.cm = max_drop_nan(A.cm, fabs(v));
         A.nan |= (v != v);  // a NaN residual poisons its tile sum
     }
@@ -288,7 +312,9 @@ __device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int
 // partials and applies the reference's branch logic. (A single final warp
 // folding all ~5500 partials serially added a multi-microsecond tail to every
 // pass.) Scratch: part = [3 per CTA | 3 per group], ticket = [all | per group].
-__device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double mx, double sx, double cm, int nan) {
+template <bool MP>
+__device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double mx, double sx, double cm, int nan,
+                                              const Ctl& st) {
     const int nb = gridDim.x * gridDim.y;
     const int bid = blockIdx.y * gridDim.x + blockIdx.x;
     const int lane = threadIdx.x & 31;
@@ -337,9 +363,16 @@ __device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double 
     s = warp_sum_down(s);
     c = warp_max(c);
     if (lane == 0) {
-        if (P.mp) {  // all-reduced across ranks, then mp_unpack_kernel decides
-            P.rank_part[0] = m, P.rank_part[1] = c, P.rank_part[2] = 1.0, P.rank_part[3] = double(mode);
-            P.rank_part[4] = s;
+        if constexpr (MP) {  // to every rank's pack slot, then raise this rank's flag on every rank
+            const int p = int(st.mp_seq & 1ull);
+            double* mine = P.xch[P.rank] + (int64_t(p) * P.nranks + P.rank) * P.pack_len;
+            mine[0] = m, mine[1] = c, mine[2] = 1.0, mine[3] = double(mode), mine[4] = s;
+            fence_release_sys();  // with the tickets' chain: this pass's whole slot before the flags
+#ifdef ISMG_MP_TRACE
+            P.ctl->mp_t1 = (unsigned long long)gtimer();
+#endif
+            for (int q = 0; q < P.nranks; ++q)
+                atomicExch(P.xflag[q] + P.rank, st.mp_seq + 1ull);  // mp_unpack_kernel waits for these
         } else {
             fine_decide(P, mode, m, s, c);
         }
@@ -361,13 +394,14 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
-    if (MP) halo_geo(G, P, L.c0);
+    const int mpp = int(st.mp_seq & 1ull);  // multi-GPU: this pass's pack parity
+    double* mpk = MP ? my_pack(P, mpp) : nullptr;
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
     auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
-        return MP ? row_src(P, xin, k, a - 4) : xin + int64_t(k) * G.pitch + (a - 4);
+        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1) : xin + int64_t(k) * G.pitch + (a - 4);
     };
     const int kfirst = G.r0 - 3, klast = G.r1 + 2;
     if ((threadIdx.x & 31) == 0) {
@@ -391,7 +425,7 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
         mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
         step_w<U, (U & 1), MP>(sm, slot, L, G, w, A, k);
         const int j = k - 3;  // tile row-block of row k-3 complete
-        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<MP>(P, L, j, lg, A, mpk);
         __syncwarp();  // every lane has read the slot of row k
         if (k + kRingW <= klast)
             issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
@@ -405,7 +439,8 @@ __device__ __forceinline__ void sweep_w(SmemW& sm, const Params& P, const Ctl& s
         if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, kb + 2);
         if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, kb + 3);
     }
-    warp_epilogue(P, kFine, A.mx, A.sx, A.cm, A.nan);
+    if (MP) mp_push(P, L, G, mpp, G.outp);
+    warp_epilogue<MP>(P, kFine, A.mx, A.sx, A.cm, A.nan, st);
 }
 
 // ---- PROLONG / RESID: x' = x + c + P ce (coarsening.hpp:495-500), residual and
@@ -422,13 +457,14 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
     G.outp = st.buf[st.cur ^ 1] + L.c0;
     G.pitch = P.pitch;
-    if (MP) halo_geo(G, P, L.c0);
+    const int mpp = int(st.mp_seq & 1ull);  // multi-GPU: this pass's pack parity
+    double* mpk = MP ? my_pack(P, mpp) : nullptr;
     const int tmask = P.tile - 1, lg = ilog2(P.tile);
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
     auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
-        return MP ? row_src(P, xin, k, a - 4) : xin + int64_t(k) * G.pitch + (a - 4);
+        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1) : xin + int64_t(k) * G.pitch + (a - 4);
     };
     Acc A;
     // TileAxis::locate_cell of the lane's columns
@@ -499,9 +535,9 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
             A.sx = A.sx + ((x1[0] + x1[1]) + (x1[2] + x1[3]));
             A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
-            if (prolong) put_row<MP>(G, L, j, x1);
+            if (prolong) put_row(G, L, j, x1);
         }
-        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w(P, L, j, lg, A);
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<MP>(P, L, j, lg, A, mpk);
 #pragma unroll
         for (int q = 0; q < 4; ++q) x2[q] = x1[q], x1[q] = x0[q], b1[q] = b0[q];
         __syncwarp();
@@ -509,13 +545,18 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
             issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     }
-    warp_epilogue(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan);
+    if (MP) mp_push(P, L, G, mpp, prolong ? G.outp : xin + L.c0);
+    warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
 }
 
 template <bool MP>
 __global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : ISMG_FINE_MINB) fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
+#ifdef ISMG_MP_TRACE
+    if (MP && threadIdx.x == 0 && (st.phase == kFine || st.phase == kProlong || st.phase == kResid))
+        atomicMin(&P.ctl->mp_t0, (unsigned long long)gtimer());
+#endif
     if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
     else if (st.phase == kProlong) prolong_w<MP>(sm, P, st, nq, true);
     else if (st.phase == kResid) prolong_w<MP>(sm, P, st, nq, false);

@@ -30,9 +30,12 @@ struct FusedEngine {
     int fine_kind = 0;  // 0 column pairs (256-column CTA strips), 2 one-warp strips of column quads
     dim3 grid;
     cudaEvent_t ev = nullptr;
-    // multi-GPU strip decomposition (P.mp): this rank's pack and all ranks' packs
-    double* pack = nullptr;
-    double* gathered = nullptr;
+    // multi-GPU strip decomposition (P.mp): this rank's exchange buffer, the
+    // peers' buffers mapped through CUDA IPC, the pass counter across solves
+    char* xbuf = nullptr;
+    void* peer_map[kMaxRanks] = {};
+    double* bar_scratch = nullptr;
+    unsigned long long mp_seq = 0;
     std::vector<std::pair<int, int>> fine_rows, coarse_rows;  // per rank
 };
 
@@ -53,11 +56,12 @@ static void launch_fine(const FusedEngine& e, cudaStream_t st) {
     else launch_fine_pass(e.P, e.grid, e.smem, st);
 }
 
-// multi-GPU, after every fine-pass slot: all-reduce the pass partials (MAX of
-// max|r|, max|tile sum|, flag, mode; SUM of sum x), gather every rank's coarse
-// rhs rows, apply the branch logic, refresh the halo rows.
+// multi-GPU, after every fine-pass slot: the fine pass has stored its pack into
+// every rank's exchange buffer (NVLink peer stores) and raised its flags;
+// mp_unpack_kernel waits for all ranks' flags, reduces the pass partials in rank
+// order, assembles the coarse rhs and applies the branch logic. No NCCL call.
 static void mp_exchange(FusedEngine& e, Ctx& c) {
-    comm_allgather(*c.comm, e.pack, e.gathered, size_t(e.P.pack_len), c.stream);
+    (void)c;
     launch_mp_unpack(e.P, c.stream);
 }
 
@@ -125,6 +129,7 @@ FusedEngine* make_fused(Solver& s) {
         P.nranks = R;
         // pack = [8 scalars | this rank's coarse rows (pitched) | 3 first rows | 3 last rows]
         const int rank = c.comm->rank;
+        if (R > kMaxRanks) fail(ISMG_ERR_INVALID_ARGUMENT, "multi-GPU: more ranks than supported");
         const int64_t cpitch = L.b->view().pitch;
         int maxc = 0;
         for (auto& cr : e->coarse_rows) maxc = std::max(maxc, cr.second - cr.first);
@@ -133,18 +138,41 @@ FusedEngine* make_fused(Solver& s) {
         int64_t len = 8 + cbr + 6 * P.pitch;
         len = (len + 15) / 16 * 16;
         P.pack_len = int(len);
-        ISMG_CUDA(cudaMalloc(&e->pack, sizeof(double) * size_t(len)));
-        ISMG_CUDA(cudaMemset(e->pack, 0, sizeof(double) * size_t(len)));
-        ISMG_CUDA(cudaMalloc(&e->gathered, sizeof(double) * size_t(len) * size_t(R)));
-        ISMG_CUDA(cudaMemset(e->gathered, 0, sizeof(double) * size_t(len) * size_t(R)));
-        P.rank_part = e->pack;
-        P.gathered = e->gathered;
+        P.rank = rank;
+        P.nranks = R;
         const int cr0 = e->coarse_rows[size_t(rank)].first;
-        P.cbw = View{e->pack + 8 - int64_t(cr0) * cpitch, cpitch, L.h.ncx, L.h.ncy};
-        P.halo_send[0] = e->pack + 8 + cbr;
-        P.halo_send[1] = e->pack + 8 + cbr + 3 * P.pitch;
-        P.halo_recv[0] = rank > 0 ? e->gathered + int64_t(rank - 1) * len + 8 + cbr + 3 * P.pitch : nullptr;
-        P.halo_recv[1] = rank + 1 < R ? e->gathered + int64_t(rank + 1) * len + 8 + cbr : nullptr;
+        P.cb_off = 8 - int64_t(cr0) * cpitch, P.cb_pitch = cpitch;
+        P.h_off[0] = 8 + cbr, P.h_off[1] = 8 + cbr + 3 * P.pitch;
+        // exchange buffer [2][R][len] doubles + R flags, shared with the peers by CUDA IPC
+        const size_t data = sizeof(double) * size_t(2) * size_t(R) * size_t(len);
+        const size_t bytes = data + 256;
+        ISMG_CUDA(cudaMalloc(&e->xbuf, bytes));
+        ISMG_CUDA(cudaMemset(e->xbuf, 0, bytes));
+        ISMG_CUDA(cudaMalloc(&e->bar_scratch, sizeof(double) * 8 * size_t(R)));
+        cudaIpcMemHandle_t h;
+        ISMG_CUDA(cudaIpcGetMemHandle(&h, e->xbuf));
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        ISMG_CUDA(cudaMemcpy(e->bar_scratch + 8 * rank, &h, 64, cudaMemcpyHostToDevice));
+        std::vector<double> all(size_t(8) * size_t(R));
+        double* d_all = nullptr;
+        ISMG_CUDA(cudaMalloc(&d_all, sizeof(double) * all.size()));
+        comm_allgather(*c.comm, e->bar_scratch + 8 * rank, d_all, 8, c.stream);
+        ISMG_CUDA(cudaMemcpyAsync(all.data(), d_all, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        cudaFree(d_all);
+        for (int q = 0; q < R; ++q) {
+            char* base = e->xbuf;
+            if (q != rank) {
+                cudaIpcMemHandle_t hq;
+                std::memcpy(&hq, all.data() + 8 * q, 64);
+                void* ptr = nullptr;
+                ISMG_CUDA(cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess));
+                e->peer_map[q] = ptr;
+                base = static_cast<char*>(ptr);
+            }
+            P.xch[q] = reinterpret_cast<double*>(base);
+            P.xflag[q] = reinterpret_cast<unsigned long long*>(base + data);
+        }
     }
     P.nstrips = (P.nx + width - 1) / width;
     P.nchunks = std::max(1, (P.row1 - P.row0 + P.H - 1) / P.H);
@@ -220,8 +248,10 @@ void destroy_fused(FusedEngine* e) {
     cudaFree(e->d_log);
     cudaFree(e->coarse_backup);
     cudaFree(e->tm_spec);
-    cudaFree(e->pack);
-    cudaFree(e->gathered);
+    for (void* p : e->peer_map)
+        if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(e->xbuf);
+    cudaFree(e->bar_scratch);
     cudaFree(e->d_ctl);
     cudaFreeHost(e->h_ctl);
     if (e->ev) cudaEventDestroy(e->ev);
@@ -284,19 +314,25 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     init.buf[0] = x.buf.origin();
     init.buf[1] = e.scratch.origin();
     init.b = b.buf.origin();
+    init.mp_seq = e.mp_seq;
     *e.h_ctl = init;
     ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
-    if (e.P.mp) {  // first halo rows: this rank's boundary rows of x to the neighbours
+    if (e.P.mp) {  // first halo rows: this rank's boundary rows of x into every rank's
+                   // slot of the parity the solve's first pass reads (that of pass mp_seq - 1)
         const size_t rows3 = size_t(3) * size_t(e.P.pitch);
         const double* row0 = x.buf.origin() - kXOff;  // start of logical row 0
-        ISMG_CUDA(cudaMemsetAsync(e.pack, 0, 8 * sizeof(double), c.stream));  // no pass yet
-        if (e.P.row0 > 0)
-            ISMG_CUDA(cudaMemcpyAsync(e.P.halo_send[0], row0 + int64_t(e.P.row0) * e.P.pitch, rows3 * sizeof(double),
-                                      cudaMemcpyDeviceToDevice, c.stream));
-        if (e.P.row1 < e.P.ny)
-            ISMG_CUDA(cudaMemcpyAsync(e.P.halo_send[1], row0 + int64_t(e.P.row1 - 3) * e.P.pitch,
-                                      rows3 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-        comm_allgather(*c.comm, e.pack, e.gathered, size_t(e.P.pack_len), c.stream);
+        const int R = e.P.nranks, p = int((e.mp_seq + 1ull) & 1ull);
+        for (int q = 0; q < R; ++q) {
+            double* slot = e.P.xch[q] + (int64_t(p) * R + e.P.rank) * e.P.pack_len;
+            if (e.P.row0 > 0)
+                ISMG_CUDA(cudaMemcpyAsync(slot + e.P.h_off[0], row0 + int64_t(e.P.row0) * e.P.pitch,
+                                          rows3 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+            if (e.P.row1 < e.P.ny)
+                ISMG_CUDA(cudaMemcpyAsync(slot + e.P.h_off[1], row0 + int64_t(e.P.row1 - 3) * e.P.pitch,
+                                          rows3 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        }
+        // every rank's copies done before any rank's first pass reads them
+        comm_reduce_scalars(*c.comm, e.bar_scratch, 1, 0, c.stream);
         c.comm->collectives += 1;
     }
     // launch batches of [coarse-visit, fine-pass] slots until the phase is done
@@ -306,7 +342,6 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     for (;;) {
         ISMG_CUDA(cudaGraphLaunch(graph_for(e, slots), c.stream));
         c.launches += (e.P.mp ? 3 : 2) * slots;
-        if (c.comm && e.P.mp) c.comm->collectives += slots;
         launched_slots += slots;
         ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
         ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
@@ -326,6 +361,8 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     }
     ISMG_CUDA(cudaGetLastError());
     const Ctl& st = *e.h_ctl;
+    e.mp_seq = st.mp_seq;
+    if (st.mp_error) fail(ISMG_ERR_INTERNAL, "multi-GPU: a peer's pack did not arrive (exchange timed out)");
     // replay the sweep sequence into the metrics (lap_equiv order, metrics.hpp:46-56)
     const int nv = std::min(st.nvisits, e.P.visit_cap);
     e.h_log.resize(size_t(2) * std::max(nv, 1));

@@ -22,6 +22,8 @@ constexpr int kCoarseSmemThreads = 512;
 enum Phase : int { kFine = 0, kCoarse = 1, kProlong = 2, kResid = 3, kDone = 4 };
 
 // Device-resident solve state (one per solver).
+constexpr int kMaxRanks = 8;  // multi-GPU: ranks of one node
+
 struct Ctl {
     int phase;
     int converged;
@@ -38,6 +40,9 @@ struct Ctl {
     double r, prev, shift, rc;
     double* buf[2];
     const double* b;
+    unsigned long long mp_seq;  // multi-GPU: fine passes exchanged so far (all solves)
+    int mp_error;               // multi-GPU: a peer's pack never arrived
+    unsigned long long mp_t0, mp_t1;  // ISMG_MP_TRACE: first CTA start / last CTA end of the pass
 };
 
 struct Params {
@@ -59,29 +64,46 @@ struct Params {
     int visit_cap;
     double* coarse_scratch;  // reduction scratch for the coarse kernel
     // strip decomposition (multi-GPU): this rank relaxes fine rows [row0, row1);
-    // rows row0-3..row0-1 / row1..row1+2 come from the neighbours through
-    // halo_recv, its own first / last 3 rows go out through halo_send (3 pitched
-    // rows each, column origin kXOff). With mp set the last CTA stores the
-    // rank's partials in rank_part [max|r|, max|tile sum|, pass flag, mode, sum x]
-    // and mp_decide_kernel applies the branch logic to the all-reduced values.
+    // rows row0-3..row0-1 / row1..row1+2 are the neighbours' and arrive with
+    // their packs. A pack (pack_len doubles) = [8 scalars: max|r|, max|tile
+    // sum|, pass flag, mode, sum x | the rank's coarse-rhs rows (pitched) | its
+    // first 3 rows | its last 3 rows (pitched, column origin kXOff)].
+    // Exchange by peer stores (NVLink): every rank owns an exchange buffer
+    // [2 parities][nranks][pack_len], mapped into every rank (xch[q]). Pass s
+    // (Ctl::mp_seq) writes its pack into slot [s & 1][rank] of every rank's
+    // buffer while it computes, then raises xflag[q][rank] to s + 1 on every
+    // rank; mp_unpack_kernel waits for all ranks' flags and decides. The
+    // parities keep pass s's writes off the halo rows pass s reads (s - 1).
     int row0, row1, mp;
-    double* halo_send[2];
-    const double* halo_recv[2];
-    double* rank_part;
-    View cbw;  // where the fused pass writes its tile sums (cb; multi-GPU: the rank's pack)
-    // multi-GPU pack: per rank `pack_len` doubles = [8 scalars | coarse rows | 2 x 3 halo rows]
-    const double* gathered;  // all ranks' packs after the allgather
-    int nranks, pack_len, pack_cb_rows;
+    int rank, nranks, pack_len, pack_cb_rows;
+    double* xch[kMaxRanks];
+    unsigned long long* xflag[kMaxRanks];
+    int64_t cb_off, cb_pitch;  // pack offset of coarse cell (I, J): cb_off + J * cb_pitch + I
+    int64_t h_off[2];          // pack offsets of the first / last 3 rows
+    View cbw;                  // single GPU: where the fused pass writes its tile sums (= cb)
 };
 
 // x-row source of the fused passes: the rank's own rows from the field, the
-// neighbours' rows from the halo buffers (multi-GPU only)
-__device__ __forceinline__ const double* row_src(const Params& P, const double* xin, int k, int col) {
+// neighbours' rows from their packs of the previous pass (parity hp)
+__device__ __forceinline__ const double* row_src(const Params& P, const double* xin, int k, int col, int hp) {
     if (P.mp) {
-        if (k < P.row0 && P.row0 > 0) return P.halo_recv[0] + int64_t(k - (P.row0 - 3)) * P.pitch + kXOff + col;
-        if (k >= P.row1 && P.row1 < P.ny) return P.halo_recv[1] + int64_t(k - P.row1) * P.pitch + kXOff + col;
+        const double* x = P.xch[P.rank] + int64_t(hp) * P.nranks * P.pack_len;
+        if (k < P.row0 && P.row0 > 0)
+            return x + int64_t(P.rank - 1) * P.pack_len + P.h_off[1] + int64_t(k - (P.row0 - 3)) * P.pitch + kXOff + col;
+        if (k >= P.row1 && P.row1 < P.ny)
+            return x + int64_t(P.rank + 1) * P.pack_len + P.h_off[0] + int64_t(k - P.row1) * P.pitch + kXOff + col;
     }
     return xin + int64_t(k) * P.pitch + col;
+}
+
+// multi-GPU: one pack word of pass parity p into every rank's exchange buffer
+__device__ __forceinline__ void mp_put(const Params& P, int p, int64_t off, double v) {
+    const int64_t o = (int64_t(p) * P.nranks + P.rank) * P.pack_len + off;
+    for (int q = 0; q < P.nranks; ++q) P.xch[q][o] = v;
+}
+__device__ __forceinline__ void mp_put2(const Params& P, int p, int64_t off, double a, double b) {
+    const int64_t o = (int64_t(p) * P.nranks + P.rank) * P.pack_len + off;
+    for (int q = 0; q < P.nranks; ++q) *reinterpret_cast<double2*>(P.xch[q] + o) = make_double2(a, b);
 }
 
 __device__ __forceinline__ long long gtimer() {

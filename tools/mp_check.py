@@ -33,14 +33,15 @@ def run(ctx, n, tile, steps):
     m = RunMetrics(n * n)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    per = []
+    per, coarse = [], []
     for _ in range(steps):
         t1 = time.perf_counter()
         ds.step(solver, m)
         ctx.synchronize()
         per.append(round(time.perf_counter() - t1, 4))
+        coarse.append(round(solver.last_stats()["coarse_ms"] * 1e-3, 4))
     secs = time.perf_counter() - t0
-    print("rank", ctx.device, "per-step seconds", per, flush=True)
+    print("rank", ctx.device, "per-step seconds", per, "coarse seconds", coarse, flush=True)
     out = FluidState(g)
     ds.download(out)
     rows = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, int(r.converged)) for r in m.rows]
