@@ -47,6 +47,7 @@ namespace {
 constexpr int kLag = 8;            // wavefront steps between consecutive sweeps
 constexpr int kMaxGroup = 512;     // sweeps per checkpointed group
 constexpr int kPredCap = 32;       // cap of the predicted first group of a visit
+constexpr int kHandG = 4;          // role 1: largest group run on one SM
 constexpr int kIntWarps = 16;     // warps: 4 row blocks x 4 sweeps in flight
 constexpr int kClThreads = 32 * kIntWarps;
 
@@ -346,6 +347,15 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
     __shared__ ClShared cs;
     Ctl* st = P.ctl;
     if (st->phase != kCoarse) return;
+    if (T.role == 2 && st->cl_hand == 0) return;  // the one-SM kernel finished this visit
+    if (T.role == 1 && max(1, min(st->pred, kPredCap)) > kHandG) {  // a long visit: all of it on the cluster
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            st->cl_hand_G = max(1, min(st->pred, kPredCap)), st->cl_hand_done = 0, st->cl_hand_rc = st->rc;
+            st->cl_hand = 1;
+        }
+        return;
+    }
     const long long t_start = gtimer();
     cg::cluster_group cluster = cg::this_cluster();
     double* dyn = cl_dyn;
@@ -366,7 +376,8 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
     B.south = (B.c > 0) ? cluster.map_shared_rank(B.xs, B.c - 1) + size_t(R + 1) * pitch + 1 : nullptr;
     B.north = (B.c + 1 < B.C && B.J1 < T.ncy) ? cluster.map_shared_rank(B.xs, B.c + 1) + 1 : nullptr;
     const int nxs = rows * pitch;
-    for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = 0.0;  // ce = 0, zero ghosts and halos
+    if (BM != 2)  // (BM == 2: zeroed after the rhs staging that borrows the area)
+        for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = 0.0;  // ce = 0, zero ghosts and halos
     B.tmem = 0;
     if constexpr (BM == 2) {  // rhs into Tensor Memory: 512 columns = 256 fp64 diagonal slots per row
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -379,15 +390,25 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
         __syncthreads();
         tm_fence_after();
         B.tmem = uint32_t(cs.ictl[3]);
+        // the band's rhs rows through the (not yet zeroed) iterate area with
+        // coalesced loads, then from shared memory along the diagonal slots
+        double* tmp = B.xs;  // row jj at tmp + jj * T.bpitch
+        for (int k = threadIdx.x; k < (B.J1 - B.J0) * T.ncx; k += blockDim.x) {
+            const int jj = k / T.ncx, I = k - jj * T.ncx;
+            tmp[jj * T.bpitch + I] = P.cb.at(I, B.J0 + jj);
+        }
+        __syncthreads();
         const int q = warp & 3, nh = int(blockDim.x >> 7);
         const int J = B.J0 + 32 * q + lane;
         const uint32_t tq = B.tmem + (uint32_t(32 * q) << 16);
         for (int slot = warp >> 2; slot < 256; slot += nh) {
             const int I = (slot - 2 * J) & 255;
-            const double v = (J < B.J1 && I < T.ncx) ? P.cb.at(I, J) : 0.0;
+            const double v = (J < B.J1 && I < T.ncx) ? tmp[(J - B.J0) * T.bpitch + I] : 0.0;
             tm_st2(tq + 2u * uint32_t(slot), uint32_t(__double2loint(v)), uint32_t(__double2hiint(v)));
         }
         tm_wait_st();
+        __syncthreads();
+        for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = 0.0;
         tm_fence_before();
         __syncthreads();
         tm_fence_after();
@@ -399,15 +420,32 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
         }
     const int spec_words = 10 * (T.ncls + 1) + (T.ring + 1) / 2;
     for (int k = threadIdx.x; k < spec_words; k += blockDim.x) spec[k] = spec_g[k];
+    const bool resume = T.role == 2;
+    if (resume && st->cl_hand_done > 0)  // the handed-over iterate, band and halo rows
+        for (int k = threadIdx.x; k < rows * T.ncx; k += blockDim.x) {
+            const int jj = k / T.ncx, I = k - jj * T.ncx, J = B.J0 - 1 + jj;
+            if (J >= 0 && J < T.ncy && J <= B.J1) B.xs[jj * pitch + 1 + I] = P.ce.at(I, J);
+        }
     cluster.sync();
     double* my_backup = backup + size_t(B.c) * nxs;
-    double rc = st->rc;  // max|cb|, formed by the fine pass that restricted
+    double rc = resume ? st->cl_hand_rc : st->rc;  // max|cb|, formed by the fine pass that restricted
     const long long budget = P.max_total - st->total;
-    long long done = 0, steps = 0, gns = 0;
+    long long done = resume ? st->cl_hand_done : 0, steps = 0, gns = 0;
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
-    int G = max(1, min(st->pred, kPredCap));
+    int G = resume ? st->cl_hand_G : max(1, min(st->pred, kPredCap));
+    if (resume) {
+        cluster.sync();  // every CTA has read the hand-over before it is cleared
+        if (B.c == 0 && threadIdx.x == 0) st->cl_hand = 0;
+    }
+    bool handoff = false;
     while (rc > P.tol_coarse && done < budget) {
         if (budget - done < G) G = int(budget - done);
+        // one SM is faster while every warp owns one sweep (G <= 4 at 128 rows); larger
+        // groups go to the cluster kernel that follows in the same graph slot
+        if (T.role == 1 && G > kHandG) {
+            handoff = true;
+            break;
+        }
         if (G > 1)
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) my_backup[k] = B.xs[k];  // checkpoint
         const long long tg0 = gtimer();
@@ -467,7 +505,7 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
         G = min(2 * G, kMaxGroup);
     }
     // anchor once (singular) and hand ce to the prolongation
-    if (P.singular && done > 0) {
+    if (P.singular && done > 0 && !handoff) {
         double sum = 0.0;
         for (int J = B.J0 + int(threadIdx.x >> 5); J < B.J1; J += int(blockDim.x >> 5)) {
             const double* r = B.xs + (J - B.J0 + 1) * pitch + 1;
@@ -498,6 +536,16 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
         if ((threadIdx.x >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(B.tmem));
     }
     cluster.sync();  // no CTA exits while another may still read its shared memory
+    if (handoff) {
+        if (B.c == 0 && threadIdx.x == 0) {
+            st->coarse_ns += gtimer() - t_start;
+            st->coarse_steps += steps;
+            st->coarse_group_ns += gns;
+            st->cl_hand_G = G, st->cl_hand_done = done, st->cl_hand_rc = rc;
+            st->cl_hand = 1;
+        }
+        return;
+    }
     if (B.c == 0 && threadIdx.x == 0) {
         st->coarse_launches += 1;
         st->coarse_ns += gtimer() - t_start;
@@ -549,7 +597,7 @@ void set_attrs(size_t smem) {
 
 // Host plan: stencil classes (interior constant + tabulated boundary ring),
 // cluster size and band height so the band fits shared memory.
-bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem) {
+bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem, int band_min) {
     if (op.px || op.py || op.ncx < 3 || op.ncy < 3) return false;
     T.ncx = op.ncx, T.ncy = op.ncy, T.five = op.five_point;
     T.ring = 2 * op.ncx + 2 * op.ncy;
@@ -613,6 +661,7 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
         }
     }
     T.kind = (T.five ? 1 : 0) | (zghost ? 0 : 2);
+    T.role = 0;
     // table: classes 0..ncls-1 (ring), class ncls (interior), then the ring's class ids
     spec.assign(size_t(10) * (T.ncls + 1) + size_t(T.ring + 1) / 2, 0.0);
     for (int c = 0; c <= T.ncls; ++c) {
@@ -632,7 +681,7 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     // flight up (measured at 128^2: 252 ms of coarse groups at C = 4 against 346 at
     // C = 1 over a 4096^2 step). rhs in shared memory if it fits, else in Tensor
     // Memory (bands <= 128 rows, ncx <= 256), else read through L1.
-    int rmin = 32;  // tuning hook: ISMG_CL_BAND = smallest band height tried
+    int rmin = std::max(32, band_min / 32 * 32);  // tuning hook: ISMG_CL_BAND = smallest band height tried
     if (const char* e = getenv("ISMG_CL_BAND")) rmin = std::max(32, atoi(e) / 32 * 32);
     for (int R = rmin; R <= 32 * kMaxRowBlocks; R *= 2) {
         const int C = (op.ncy + R - 1) / R;

@@ -25,6 +25,12 @@ struct FusedEngine {
     int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands
     TmGeom tm{};
     ClGeom cl{};
+    // hybrid coarse visits: a one-SM kernel (cl1, role 1) runs groups of <= 4
+    // sweeps and hands larger ones to the cluster kernel (cl, role 2)
+    bool cl_hybrid = false;
+    ClGeom cl1{};
+    size_t coarse_smem1 = 0;
+    double* coarse_backup1 = nullptr;
     double* tm_spec = nullptr;
     size_t smem = 0;
     int fine_kind = 0;  // 0 column pairs (256-column CTA strips), 2 one-warp strips of column quads
@@ -76,6 +82,8 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     cudaGraph_t g;
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
+        if (e.coarse_kind == 3 && e.cl_hybrid)
+            launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
         if (e.coarse_kind == 3)
             launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
         else if (e.coarse_kind == 2)
@@ -221,7 +229,22 @@ FusedEngine* make_fused(Solver& s) {
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
         ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
         ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * cl_backup_doubles(e->cl)));
-        set_coarse_cl_smem(e->coarse_smem);
+        size_t smax = e->coarse_smem;
+        // hybrid when the grid also fits one SM and the cluster is 2 SMs: a 2048^2
+        // step 1 takes 170 ms with it against 181 without; at 4096^2 (4 SMs) the
+        // one-SM kernel's shorter small groups are eaten by the extra launch per
+        // slot (494 against 487 ms). ISMG_CL_HYBRID=0 / 1 forces it off / on.
+        const char* hy = getenv("ISMG_CL_HYBRID");
+        const bool want = hy ? std::string(hy) != "0" : e->cl.csize == 2;
+        std::vector<double> spec1;
+        if (e->cl.csize > 1 && want &&
+            cl_coarse_plan(L.h, e->cl1, spec1, e->coarse_smem1, 128) && e->cl1.csize == 1 && spec1 == spec) {
+            e->cl_hybrid = true;
+            e->cl1.role = 1, e->cl.role = 2;
+            ISMG_CUDA(cudaMalloc(&e->coarse_backup1, sizeof(double) * cl_backup_doubles(e->cl1)));
+            smax = std::max(smax, e->coarse_smem1);
+        }
+        set_coarse_cl_smem(smax);
     } else if (allow_tmem && tmem_coarse_plan(L.h, e->tm, spec, e->coarse_smem)) {
         e->coarse_kind = 2;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
@@ -248,6 +271,7 @@ void destroy_fused(FusedEngine* e) {
     cudaFree(e->d_log);
     cudaFree(e->coarse_backup);
     cudaFree(e->tm_spec);
+    cudaFree(e->coarse_backup1);
     for (void* p : e->peer_map)
         if (p) cudaIpcCloseMemHandle(p);
     cudaFree(e->xbuf);
@@ -341,7 +365,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     int since_poll = 0;
     for (;;) {
         ISMG_CUDA(cudaGraphLaunch(graph_for(e, slots), c.stream));
-        c.launches += (e.P.mp ? 3 : 2) * slots;
+        c.launches += (e.P.mp ? 3 : 2) * slots + (e.cl_hybrid ? slots : 0);
         launched_slots += slots;
         ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
         ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
@@ -391,7 +415,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.coarse_steps = st.coarse_steps;
     s.last.collectives = c.comm ? c.comm->collectives : 0;
     s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
-    s.last.kernel_launches = (e.P.mp ? 3 : 2) * launched_slots + 2;
+    s.last.kernel_launches = ((e.P.mp ? 3 : 2) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;
 }
 
 }  // namespace ismgb

@@ -43,6 +43,11 @@ struct Ctl {
     unsigned long long mp_seq;  // multi-GPU: fine passes exchanged so far (all solves)
     int mp_error;               // multi-GPU: a peer's pack never arrived
     unsigned long long mp_t0, mp_t1;  // ISMG_MP_TRACE: first CTA start / last CTA end of the pass
+    // coarse visit handed from the one-SM kernel to the cluster kernel at a group
+    // boundary (iterate in ce): next group size, sweeps done, residual
+    int cl_hand, cl_hand_G;
+    long long cl_hand_done;
+    double cl_hand_rc;
 };
 
 struct Params {
@@ -320,11 +325,12 @@ struct ClGeom {
     int csize, band;    // cluster size (CTAs), rows per CTA band
     int bsmem;          // rhs: 1 shared memory, 2 Tensor Memory, 0 read through L1
     int ring, ncls, fastdiv, kind;
+    int role;  // 0: whole visits; 1: one-SM kernel, hands groups above 4 sweeps on; 2: cluster kernel, resumes them
     bool five;
     double stdw[9];  // interior weights (slot order C, E, W, N, S, NE, NW, SE, SW)
     double stdy;     // RN(1 / stdw[0]): Markstein's reciprocal (fastdiv)
 };
-bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem);
+bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem, int band_min = 0);
 size_t cl_backup_doubles(const ClGeom& T);
 void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
                       cudaStream_t st);

@@ -163,3 +163,29 @@ def test_coarse_visit_kernels_match_oracle(dev, port, monkeypatch, kernel, which
     for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
                  (res.state.p.data, st.p.data)):
         assert rel_l2(a, b) <= REL_L2
+
+
+@pytest.mark.parametrize("env", [{}, {"ISMG_CL_HYBRID": "0"}, {"ISMG_CL_HYBRID": "1"}, {"ISMG_CL_BAND": "64"},
+                                 {"ISMG_CL_BAND": "128"}])
+def test_coarse_cluster_plans_match_oracle(dev, port, monkeypatch, env):
+    """The cluster coarse kernel on a 64x64 coarse grid under every plan: 32-row
+    bands on 2 SMs with the one-SM hand-off (default) or without it, 64-row bands
+    on one SM, and a forced hybrid. Per-step counts equal the reference's."""
+    P = dev
+    monkeypatch.setenv("ISMG_COARSE_KERNEL", "cl")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    case = setup_lid_cavity(256, 1000.0)
+    case.dt = 1000.0 / 256
+    cfg, nsteps = CycleConfig(tile=4), 3
+    case.steps, case.t_max, case.steady_tol = nsteps, 0.0, 0.0
+    res = P.run_case(case, cfg)
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, _ = port.run_steps(case.grid, cfg, st, nsteps)
+    got = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in res.metrics.rows]
+    want = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in rows]
+    assert got == want
+    for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
+                 (res.state.p.data, st.p.data)):
+        assert rel_l2(a, b) <= REL_L2
