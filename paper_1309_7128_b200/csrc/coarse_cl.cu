@@ -184,7 +184,7 @@ __device__ __forceinline__ double apply_lane(const Wts& W, const Nbr& v, double 
 // the class table only when the cell's class changes (ring cells: first / last
 // row and column; the interior is class ncls), so ring cells cost no extra pass.
 template <int Kind, int BM>
-__device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G, bool residuals) {
+__device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G, bool residuals) {
     constexpr bool kFive = (Kind & 1) != 0, kSel = (Kind & 2) != 0;
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -228,7 +228,18 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
         for (int k = threadIdx.x; k < nrb * kMaxGroup; k += blockDim.x) (&cs.cmax[0][0])[k] = 0.0;
     }
     __syncthreads();
-    const int tau_end = dmax + kLag * (G - 1) + (residuals ? 4 : 0);
+    // Schedule: sweep g updates cell (I, J) of band c at step I + 2J + L g + D c and
+    // forms its residual R steps later. One SM, or bands of several row blocks: a
+    // barrier every step, L = 8, R = 4, D = 0. A cluster of 32-row bands keeps every
+    // sweep of a band in one warp, so only other sweeps and the band edges need
+    // the cluster. Skewing the bands by D = 1 step, with R = 6 and L = 12, puts
+    // every such dependency (RAW and WAR, including the mirrored halo rows) >= 2
+    // steps apart, so a cluster barrier every S = 2 steps suffices, with a warp
+    // barrier in between.
+    const bool s2 = B.C > 1 && nrb == 1;
+    const int L = s2 ? 12 : kLag, R = s2 ? 6 : 4, D = s2 ? 1 : 0, S = s2 ? 2 : 1;
+    const int toff = D * B.c;
+    const int tau_end = dmax + D * (B.C - 1) + L * (G - 1) + (residuals ? R : 0);
     const int dlo = 2 * Jw, dhi = 2 * jlast + T.ncx - 1;
     // G <= kH: every warp of a row block owns at most one sweep (g = h) for the
     // whole group, so its residual max stays in a register until the group ends
@@ -295,26 +306,26 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
         };
         if (w_on) {
             if (one_g) {  // this warp's only sweep is g = h
-                const int dU = tau - kLag * h, dR = dU - 4;
+                const int dU = tau - toff - L * h, dR = dU - R;
                 const bool du = h < G && dU >= dlo && dU <= dhi;
                 const bool dres = residuals && h < G && dR >= dlo && dR <= dhi;
                 if (du || dres) pair(du, dres, dU, dR, h);
             } else {
-                const int bu0 = tau, br0 = residuals ? tau - 4 : -1;
+                const int bu0 = tau - toff, br0 = residuals ? tau - toff - R : -1;
                 int gu = 0, guh = -1, gr = 0, grh = -1;
                 if (bu0 >= dlo) {
-                    const int g_lo = max(0, (bu0 - dhi + kLag - 1) >> 3);
-                    guh = min(G - 1, (bu0 - dlo) >> 3);
+                    const int g_lo = max(0, (bu0 - dhi + L - 1) / L);
+                    guh = min(G - 1, (bu0 - dlo) / L);
                     gu = g_lo + ((h - g_lo) & (kH - 1));
                 }
                 if (br0 >= dlo) {
-                    const int g_lo = max(0, (br0 - dhi + kLag - 1) >> 3);
-                    grh = min(G - 1, (br0 - dlo) >> 3);
+                    const int g_lo = max(0, (br0 - dhi + L - 1) / L);
+                    grh = min(G - 1, (br0 - dlo) / L);
                     gr = g_lo + ((h - g_lo) & (kH - 1));
                 }
 #pragma unroll 1
                 while (gu <= guh || gr <= grh) {
-                    pair(gu <= guh, gr <= grh, bu0 - kLag * gu, br0 - kLag * gr, gr);
+                    pair(gu <= guh, gr <= grh, bu0 - L * gu, br0 - L * gr, gr);
                     gu += kH, gr += kH;
                 }
             }
@@ -323,7 +334,8 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
         const long long c1 = clock64();
         tr_int += c1 - c0;
 #endif
-        step_sync(B);
+        if (S == 1 || tau % S == S - 1 || tau == tau_end) step_sync(B);
+        else __syncwarp();
 #ifdef ISMG_CL_TRACE
         tr_bar += clock64() - c1;
 #endif
@@ -339,6 +351,7 @@ __device__ void cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShar
         printf("TRACE G=%d steps=%d warp=%2d loop=%lld int=%lld bar=%lld\n", G, tau_end + 1, warp, tr_loop, tr_int,
                tr_bar);
 #endif
+    return tau_end + 1;
 }
 
 template <int Kind, int BM>
@@ -431,7 +444,6 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
     double rc = resume ? st->cl_hand_rc : st->rc;  // max|cb|, formed by the fine pass that restricted
     const long long budget = P.max_total - st->total;
     long long done = resume ? st->cl_hand_done : 0, steps = 0, gns = 0;
-    const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
     int G = resume ? st->cl_hand_G : max(1, min(st->pred, kPredCap));
     if (resume) {
         cluster.sync();  // every CTA has read the hand-over before it is cleared
@@ -452,12 +464,12 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
 #ifdef ISMG_CL_TRACE
         const long long ck0 = clock64();
 #endif
-        cl_group<Kind, BM>(T, B, P.cb, cs, G, true);
+        const int gsteps = cl_group<Kind, BM>(T, B, P.cb, cs, G, true);
         gns += gtimer() - tg0;
 #ifdef ISMG_CL_TRACE
         if (threadIdx.x == 0 && B.c == 0) printf("GROUP G=%d ns=%lld cycles=%lld\n", G, gtimer() - tg0, clock64() - ck0);
 #endif
-        steps += dmax + kLag * (G - 1) + 5;
+        steps += gsteps;
         // cluster-wide first sweep whose residual passes tol_coarse
         {
             const int nrb = (B.J1 - B.J0 + 31) >> 5;
@@ -491,12 +503,11 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = my_backup[k];
             cluster.sync();
             const long long tg0 = gtimer();
-            cl_group<Kind, BM>(T, B, P.cb, cs, first + 1, false);
+            steps += cl_group<Kind, BM>(T, B, P.cb, cs, first + 1, false);
             gns += gtimer() - tg0;
 #ifdef ISMG_CL_TRACE
             if (threadIdx.x == 0 && B.c == 0) printf("REPLAY G=%d ns=%lld\n", first + 1, gtimer() - tg0);
 #endif
-            steps += dmax + kLag * first + 1;
             done += first + 1;
             break;
         }
