@@ -48,6 +48,12 @@ constexpr int kLag = 8;            // wavefront steps between consecutive sweeps
 constexpr int kMaxGroup = 512;     // sweeps per checkpointed group
 constexpr int kPredCap = 32;       // cap of the predicted first group of a visit
 constexpr int kHandG = 4;          // role 1: largest group run on one SM
+#ifndef ISMG_CL_S4
+#define ISMG_CL_S4 3  // barrier interval on a 4-SM cluster (tuning hook)
+#endif
+#ifndef ISMG_CL_S8
+#define ISMG_CL_S8 4  // ... on 8 or more SMs
+#endif
 constexpr int kIntWarps = 16;     // warps: 4 row blocks x 4 sweeps in flight
 constexpr int kClThreads = 32 * kIntWarps;
 
@@ -183,7 +189,7 @@ __device__ __forceinline__ double apply_lane(const Wts& W, const Nbr& v, double 
 // of its current update and residual cells in registers and reloads them from
 // the class table only when the cell's class changes (ring cells: first / last
 // row and column; the interior is class ncls), so ring cells cost no extra pass.
-template <int Kind, int BM>
+template <int Kind, int BM, int S>
 __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G, bool residuals) {
     constexpr bool kFive = (Kind & 1) != 0, kSel = (Kind & 2) != 0;
     const int dmax = (T.ncx - 1) + 2 * (T.ncy - 1);
@@ -231,15 +237,18 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
     // Schedule: sweep g updates cell (I, J) of band c at step I + 2J + L g + D c and
     // forms its residual R steps later. One SM, or bands of several row blocks: a
     // barrier every step, L = 8, R = 4, D = 0. A cluster of 32-row bands keeps every
-    // sweep of a band in one warp, so only other sweeps and the band edges need
-    // the cluster. Skewing the bands by D = 1 step, with R = 6 and L = 12, puts
-    // every such dependency (RAW and WAR, including the mirrored halo rows) >= 2
-    // steps apart, so a cluster barrier every S = 2 steps suffices, with a warp
-    // barrier in between.
-    // (for every group size: limited to one-sweep-per-warp groups it measured slower,
-    // 4096^2 step 1 494 against 481 ms, 16384^2 probe 33.2 against 28.1 ms)
-    const bool s2 = B.C > 1 && nrb == 1;
-    const int L = s2 ? 12 : kLag, R = s2 ? 6 : 4, D = s2 ? 1 : 0, S = s2 ? 2 : 1;
+    // sweep of a band in one warp, so only other sweeps and the band edges need the
+    // cluster. Skewing the bands by D steps and stretching R and L puts every such
+    // dependency (RAW and WAR, the mirrored halo rows included) >= S steps apart,
+    // so a cluster barrier every S steps suffices, with a warp barrier in between.
+    // (S = 2: D = 1, R = 6, L = 12; the binding constraints are the last row's
+    // residual reading the next band's NE, R >= 3 + D + S, and the next sweep
+    // overwriting the previous band's SW after the residual read it,
+    // L >= R + D + S + 3.)
+    // A barrier every S steps (S > 1: clusters of 32-row bands only):
+    // D = S - 1, R = 3 + D + S, L = R + D + S + 3; compile-time, so the sweep-range
+    // divisions by L and the step test are shifts and masks where they can be.
+    constexpr int D = S - 1, R = S > 1 ? 3 + D + S : 4, L = S > 1 ? R + D + S + 3 : kLag;
     const int toff = D * B.c;
     const int tau_end = dmax + D * (B.C - 1) + L * (G - 1) + (residuals ? R : 0);
     const int dlo = 2 * Jw, dhi = 2 * jlast + T.ncx - 1;
@@ -336,7 +345,7 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
         const long long c1 = clock64();
         tr_int += c1 - c0;
 #endif
-        if (S == 1 || tau % S == S - 1 || tau == tau_end) step_sync(B);
+        if (S == 1 || tau % S == S - 1 || tau == tau_end) step_sync(B);  // S: template constant
         else __syncwarp();
 #ifdef ISMG_CL_TRACE
         tr_bar += clock64() - c1;
@@ -354,6 +363,21 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
                tr_bar);
 #endif
     return tau_end + 1;
+}
+
+// The barrier interval of a group: 1 on one SM or with multi-block bands; on a
+// cluster of 32-row bands 2 on 2 SMs, 3 on 4, 4 from 8. Measured (same box, A/B):
+// 4096^2 (4 SMs) coarse per step 1 / 2: 214 / 85 ms at S = 3, 219 / 89 at S = 2,
+// 213 / 84 at S = 4; 16384^2 (16 SMs) per 200-sweep visit: 22.1 ms at S = 4,
+// 21.4 at S = 5, 32.9 at S = 1.
+template <int Kind, int BM>
+__device__ __forceinline__ int cl_group_s(const ClGeom& T, const Band& B, const View& cbg, ClShared& cs, int G,
+                                          bool residuals) {
+    const bool bands = B.C > 1 && B.J1 - B.J0 <= 32;
+    if (!bands) return cl_group<Kind, BM, 1>(T, B, cbg, cs, G, residuals);
+    if (B.C >= 8) return cl_group<Kind, BM, ISMG_CL_S8>(T, B, cbg, cs, G, residuals);
+    if (B.C >= 4) return cl_group<Kind, BM, ISMG_CL_S4>(T, B, cbg, cs, G, residuals);
+    return cl_group<Kind, BM, 2>(T, B, cbg, cs, G, residuals);
 }
 
 template <int Kind, int BM>
@@ -466,7 +490,7 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
 #ifdef ISMG_CL_TRACE
         const long long ck0 = clock64();
 #endif
-        const int gsteps = cl_group<Kind, BM>(T, B, P.cb, cs, G, true);
+        const int gsteps = cl_group_s<Kind, BM>(T, B, P.cb, cs, G, true);
         gns += gtimer() - tg0;
 #ifdef ISMG_CL_TRACE
         if (threadIdx.x == 0 && B.c == 0) printf("GROUP G=%d ns=%lld cycles=%lld\n", G, gtimer() - tg0, clock64() - ck0);
@@ -505,7 +529,7 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
             for (int k = threadIdx.x; k < nxs; k += blockDim.x) B.xs[k] = my_backup[k];
             cluster.sync();
             const long long tg0 = gtimer();
-            steps += cl_group<Kind, BM>(T, B, P.cb, cs, first + 1, false);
+            steps += cl_group_s<Kind, BM>(T, B, P.cb, cs, first + 1, false);
             gns += gtimer() - tg0;
 #ifdef ISMG_CL_TRACE
             if (threadIdx.x == 0 && B.c == 0) printf("REPLAY G=%d ns=%lld\n", first + 1, gtimer() - tg0);
@@ -620,8 +644,6 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
             for (int sl = 0; sl < 9; ++sl)
                 if (!same_bits(op.at(sl, I, J), T.stdw[sl])) return false;
     if (T.stdw[0] == 0.0) return false;
-    static const double ismg[9] = {-3.0, 0.5, 0.5, 0.5, 0.5, 0.25, 0.25, 0.25, 0.25};
-    static const double five[9] = {-4.0, 1.0, 1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0};
     std::vector<std::array<double, 9>> cls;
     std::vector<int> ring_cls(size_t(T.ring), 0);
     auto classify = [&](int r, int I, int J) {
