@@ -5,9 +5,14 @@ import paper_1309_7128_b200 as P
 from paper_1309_7128_b200.api import CycleConfig, FluidState, RunMetrics, setup_lid_cavity
 
 n, tile, budget = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+tol_c = float(sys.argv[4]) if len(sys.argv) > 4 else None  # e.g. 1e-300: the visit runs the whole budget
 case = setup_lid_cavity(n, 1000.0)
 case.dt = 1000.0 / n
-solver = P.PressureSolver(case.grid, CycleConfig(tile=tile, max_total_sweeps=budget))
+cfg = CycleConfig(tile=tile, max_total_sweeps=budget)
+if tol_c is not None:
+    cfg.tol_coarse = tol_c
+    cfg.tol_fine = min(cfg.tol_fine, tol_c)
+solver = P.PressureSolver(case.grid, cfg)
 st = FluidState(case.grid); st.dt, st.nu = case.dt, case.nu
 ds = P.DeviceState(case.grid, solver.ctx, st)
 m = RunMetrics(n * n)
