@@ -255,6 +255,11 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
     // G <= kH: every warp of a row block owns at most one sweep (g = h) for the
     // whole group, so its residual max stays in a register until the group ends
     const bool one_g = G <= kH;
+#ifndef ISMG_CL_SPLIT
+#define ISMG_CL_SPLIT 1
+#endif
+    const bool split = ISMG_CL_SPLIT && residuals && 2 * G <= kH;
+    const int sg = h & (kH / 2 - 1);
     double lmax = 0.0;
 #ifdef ISMG_CL_TRACE
     long long tr_int = 0, tr_bar = 0;
@@ -315,8 +320,69 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
                 }
             }
         };
+        // split (G <= kH / 2): warp h < kH / 2 updates sweep h, warp h + kH / 2 forms
+        // its residuals, so the two fp64 chains run on separate warps
+        auto upd_only = [&](int dU) {
+            const int Iu = dU - 2 * J;
+            const bool oku = rowin && unsigned(Iu) < ncx;
+            const int Iuc = oku ? Iu : 0;
+            const int offu = ringrow ? B.so + 10 * ring_cls[rbase + Iuc]
+                                     : (Iu == 0 ? off_w : Iu == T.ncx - 1 ? off_e : off_i);
+            Wts Wu;
+            load_wts(offu, Wu);
+            double bu;
+            if constexpr (BM == 2) {
+                uint32_t lo0 = 0, hi0 = 0;
+                tm_ld2(tq + 2u * uint32_t(dU & 255), lo0, hi0);
+                tm_wait_ld();
+                bu = __hiloint2double(int(hi0), int(lo0));
+            } else if constexpr (BM == 1) {
+                bu = cl_dyn[browo + Iuc];
+            } else {
+                bu = __ldg(brow + Iuc);
+            }
+            const Nbr vu = gather(rowo + Iuc, pitch, false, kFive);
+            const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
+            if (oku) {
+                cl_dyn[rowo + Iu] = out;
+                if (mirror_s) B.south[Iu] = out;
+                if (mirror_n) B.north[Iu] = out;
+            }
+        };
+        auto res_only = [&](int dR) {
+            const int Ir = dR - 2 * J;
+            const bool okr = rowin && unsigned(Ir) < ncx;
+            const int Irc = okr ? Ir : 0;
+            const int offr = ringrow ? B.so + 10 * ring_cls[rbase + Irc]
+                                     : (Ir == 0 ? off_w : Ir == T.ncx - 1 ? off_e : off_i);
+            Wts Wr;
+            load_wts(offr, Wr);
+            double br_;
+            if constexpr (BM == 2) {
+                uint32_t lo1 = 0, hi1 = 0;
+                tm_ld2(tq + 2u * uint32_t(dR & 255), lo1, hi1);
+                tm_wait_ld();
+                br_ = __hiloint2double(int(hi1), int(lo1));
+            } else if constexpr (BM == 1) {
+                br_ = cl_dyn[browo + Irc];
+            } else {
+                br_ = __ldg(brow + Irc);
+            }
+            const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
+            const double rres = apply_lane<true, kFive, kSel>(Wr, vr, br_, fastdiv);
+            double m = okr ? fabs(rres) : 0.0;
+            m = (m != m) ? 0.0 : m;  // std::max drops NaN
+            lmax = fmax(lmax, m);
+        };
         if (w_on) {
-            if (one_g) {  // this warp's only sweep is g = h
+            if (split) {
+                const int dU = tau - toff - L * sg, dR = dU - R;
+                if (h < kH / 2) {
+                    if (sg < G && dU >= dlo && dU <= dhi) upd_only(dU);
+                } else if (sg < G && dR >= dlo && dR <= dhi) {
+                    res_only(dR);
+                }
+            } else if (one_g) {  // this warp's only sweep is g = h
                 const int dU = tau - toff - L * h, dR = dU - R;
                 const bool du = h < G && dU >= dlo && dU <= dhi;
                 const bool dres = residuals && h < G && dR >= dlo && dR <= dhi;
@@ -351,9 +417,10 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
         tr_bar += clock64() - c1;
 #endif
     }
-    if (one_g && residuals && w_on && h < G) {  // fold the per-lane maxima of sweep h
+    const int fold_g = split ? (h >= kH / 2 ? sg : -1) : h;  // the sweep whose residuals this warp formed
+    if (one_g && residuals && w_on && fold_g >= 0 && fold_g < G) {  // fold the per-lane maxima
         const double m = warp_max_nonneg(lmax);
-        if (lane == 0) cs.cmax[rb][h] = fmax(cs.cmax[rb][h], m);
+        if (lane == 0) cs.cmax[rb][fold_g] = fmax(cs.cmax[rb][fold_g], m);
     }
     __syncthreads();
 #ifdef ISMG_CL_TRACE
