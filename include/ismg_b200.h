@@ -142,7 +142,7 @@ typedef struct ismg_solve_stats {
     int64_t coarse_visits;      /* coarse-solve kernel launches with work    */
     int64_t kernel_launches;    /* all kernels launched by the solve          */
     int64_t host_syncs;         /* host <-> device round trips                */
-    int64_t collectives;        /* NCCL calls (multi-GPU)                     */
+    int64_t collectives;        /* NCCL calls (multi-GPU; not the per-pass exchange) */
     double fine_pass_ms;        /* summed CUDA-event time of fine passes      */
     double coarse_ms;           /* summed CUDA-event time of coarse visits    */
     double solve_ms;            /* CUDA-event time of the whole solve         */
@@ -167,9 +167,12 @@ int ismg_ctx_synchronize(ismg_ctx* ctx);
 /* multi-GPU (strip decomposition along y; no reference
  * counterpart — the reference is single-core). Rank 0 makes a 128-byte
  * ncclUniqueId, the caller shares it, every rank attaches it to its context
- * BEFORE creating solvers; fused solves on that context then own the rank's
- * strip of fine rows, exchange halo rows / scalars / coarse rhs over NCCL and
- * return the full solution on every rank. */
+ * BEFORE creating solvers (collective: every rank creates the same solvers in
+ * the same order). Fused solves on that context then own the rank's strip of
+ * fine rows and exchange halo rows / scalars / coarse rhs inside the fine pass
+ * through peer memory (CUDA IPC over NVLink; the ranks must be on one node with
+ * peer access), and return the full solution on every rank (NCCL, once per
+ * solve). At most 8 ranks. */
 int ismg_nccl_unique_id(void* out, size_t bytes);
 int ismg_ctx_attach_comm(ismg_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
 /* rows [r0, r1) of a rank: whole coarse tiles, as even as possible (host only) */
