@@ -165,19 +165,23 @@ def test_coarse_visit_kernels_match_oracle(dev, port, monkeypatch, kernel, which
         assert rel_l2(a, b) <= REL_L2
 
 
-@pytest.mark.parametrize("env", [{}, {"ISMG_CL_HYBRID": "0"}, {"ISMG_CL_HYBRID": "1"}, {"ISMG_CL_BAND": "64"},
-                                 {"ISMG_CL_BAND": "128"}])
-def test_coarse_cluster_plans_match_oracle(dev, port, monkeypatch, env):
-    """The cluster coarse kernel on a 64x64 coarse grid under every plan: 32-row
+@pytest.mark.parametrize("n,tile,env", [(256, 4, {}), (256, 4, {"ISMG_CL_HYBRID": "0"}),
+                                        (256, 4, {"ISMG_CL_HYBRID": "1"}), (256, 4, {"ISMG_CL_BAND": "64"}),
+                                        (256, 4, {"ISMG_CL_BAND": "128"}), (400, 4, {}), (520, 4, {}),
+                                        (520, 2, {})])
+def test_coarse_cluster_plans_match_oracle(dev, port, monkeypatch, n, tile, env):
+    """The cluster coarse kernel under every plan: on a 64x64 coarse grid 32-row
     bands on 2 SMs with the one-SM hand-off (default) or without it, 64-row bands
-    on one SM, and a forced hybrid. Per-step counts equal the reference's."""
+    on one SM, and a forced hybrid; on 100x100 four bands of 32, 32, 32 and 4 rows
+    and on 130x130 five bands (barrier every 3 steps); on 260x260 nine bands
+    (barrier every 4 steps). Per-step counts equal the reference's."""
     P = dev
     monkeypatch.setenv("ISMG_COARSE_KERNEL", "cl")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    case = setup_lid_cavity(256, 1000.0)
-    case.dt = 1000.0 / 256
-    cfg, nsteps = CycleConfig(tile=4), 3
+    case = setup_lid_cavity(n, 1000.0)
+    case.dt = 1000.0 / n
+    cfg, nsteps = CycleConfig(tile=tile), 3
     case.steps, case.t_max, case.steady_tol = nsteps, 0.0, 0.0
     res = P.run_case(case, cfg)
     st = FluidState(case.grid)
