@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Benchmark: ISM pressure solve (arXiv 1309.7128) on B200 — fine-grid cell-updates/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 4096|16384]
+
+--n 16384 runs BASELINE.json configs[2] (config 3, coarse 512^2) instead of the
+default config 2; every other setting is the same.
 
 Workload (BASELINE.json configs[1]): lid-driven
 cavity 4096^2, Re = 1000, u_lid = 0.1, h = 1, dt = Re/n, ISM two-level with
@@ -32,6 +35,7 @@ sample per core and reports the aggregate cell-updates/s.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -48,6 +52,10 @@ N_DEFAULT = 4096
 RE = 1000.0
 TILE = 32
 REF_SAMPLE_CAP = 3000  # max_total_sweeps of the bounded CPU sample (step 1)
+
+
+def config_name(n):
+    return "config 3" if n == 16384 else ("config 2" if n == 4096 else "lid %d^2" % n)
 
 
 def workload(n=N_DEFAULT):
@@ -146,13 +154,51 @@ def cpu_kind():
     return "reference" if available("reference") else "port"
 
 
+def cpu_fine_iterations(kind, n, iters):
+    """Bounded reference sample for grids whose capped step 1 never reaches a fine sweep:
+    `iters` outer fine iterations of step 1 (cycles.hpp:148-161: rbgs_sweep, fine_residual
+    into the residual field, anchor_mean, restrict_sum) on the step-1 rhs, timed on one core.
+    Returns (fine sweeps, seconds)."""
+    from pyoracle import Oracle
+    from paper_1309_7128_b200.api import FluidState, MacVelocity, ScalarField
+    case, cfg = workload(n)
+    g = case.grid
+    o = Oracle(kind)
+    st = FluidState(g)
+    o.apply_velocity_bc(g, st.vel)
+    vstar = MacVelocity(n, n)
+    o.predictor(g, st.vel, st.p, case.dt, case.nu, vstar)
+    o.apply_velocity_bc(g, vstar)
+    b = ScalarField(n, n)
+    o.divergence(g, vstar, b)
+    b.data *= g.h * g.h / case.dt
+    gt = dataclasses.replace(g, tile=cfg.tile)  # restrict_sum tiles the grid by the cycle's tile
+    x = ScalarField(n, n)
+    if kind == "reference":  # stage and fields built once inside the reference, iterations timed there
+        import ctypes as C
+        secs = C.c_double()
+        o._check(o._fn("fine_iterations")(C.byref(gt.to_c()), C.c_void_p(x.data.ctypes.data),
+                                          C.c_void_p(b.data.ctypes.data), C.c_long(iters), C.byref(secs)))
+        return iters, secs.value
+    res = ScalarField(n, n)
+    nc = (n + cfg.tile - 1) // cfg.tile
+    cb = ScalarField(nc, nc)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        o.rbgs_sweep(gt, x, b)
+        o.fine_residual(gt, x, b, res)
+        o.anchor_mean(gt, x)
+        o.restrict_sum(gt, res, cb)
+    return iters, time.perf_counter() - t0
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the unmodified reference CPU solve on all host cores."""
     if rank != 0:
         return
     import psutil
     kind = cpu_kind()
-    n = N_DEFAULT
+    n = args.n
     ncpu = os.cpu_count() or 1
     mem_gb = psutil.virtual_memory().available / 2 ** 30
     cores = max(1, min(ncpu, int(mem_gb // 2.5)))
@@ -185,7 +231,7 @@ def run_reference_arm(args, rank, world):
         "impl": "reference", "metric": "fine-grid cell-updates/s", "value": value, "unit": "cell-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "lid-driven cavity %dx%d Re=1000, ISM 32h two-level (config 2)" % (n, n),
+        "config": {"workload": "lid-driven cavity %dx%d Re=1000, ISM 32h two-level (%s)" % (n, n, config_name(n)),
                    "global_batch": 1, "seq_len": 0, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -201,7 +247,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.current_stream()
     ctx = P.Context(local_rank, stream.cuda_stream)
-    n = N_DEFAULT
+    n = args.n
     case, cfg = workload(n)
     g = case.grid
     cells = n * n
@@ -316,10 +362,14 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         kind = cpu_kind()
-        i_f, secs = cpu_sample(kind, n)
-        cpu = {"value": i_f * cells / secs, "unit": "cell-updates/s", "cores": 1, "kind": kind,
-               "sample": "step 1 of the same workload capped at %d sweeps (I_f %d in %.1f s)" % (REF_SAMPLE_CAP, i_f,
-                                                                                               secs)}
+        if n == N_DEFAULT:
+            i_f, secs = cpu_sample(kind, n)
+            smp = "step 1 of the same workload capped at %d sweeps (I_f %d in %.1f s)" % (REF_SAMPLE_CAP, i_f, secs)
+        else:  # a capped step 1 at 16384^2 spends its whole budget in the first coarse visit
+            i_f, secs = cpu_fine_iterations(kind, n, 2)
+            smp = ("%d outer fine iterations of step 1 (rbgs_sweep, fine_residual, anchor_mean, restrict_sum) "
+                   "in %.1f s" % (i_f, secs))
+        cpu = {"value": i_f * cells / secs, "unit": "cell-updates/s", "cores": 1, "kind": kind, "sample": smp}
 
     if rank == 0:
         line = {
@@ -327,18 +377,19 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (quiescent lid-driven cavity, seed 0)",
-            "config": {"workload": "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (config 2)" % (n, n),
+            "config": {"workload": "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (%s)" % (n, n, config_name(n)),
                        "global_batch": 1, "seq_len": 0,
                        "parallelism": ("y-strips x%d (halo rows pushed over NVLink by the fine pass, partials "
                                        "and coarse-rhs rows pulled from peer memory; coarse solve replicated)"
                                        % world) if dist else "single GPU",
                        "steps_timed": "projection steps 1..%d" % args.steps,
-                       "l2": "inputs larger than L2 (x, scratch, b: 3 x 134 MB vs 126 MB L2)",
+                       "l2": "inputs larger than L2 (x, scratch, b: 3 x %.0f MB vs 126 MB L2)" % (8.0 * (n + 2) ** 2 / 1e6),
                        "fine_sweeps": int(fine_all), "coarse_sweeps": int(coarse)},
+            "pressure_solves_per_s": args.steps / (ms_max * 1e-3),
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": bytes_io,
                     "d2h_bytes_per_step": bytes_io},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": fine_traffic(), "kernel": "fine_pass_w_kernel (sweep mode)",
+                         "traffic": fine_traffic() if n == 4096 else None, "kernel": "fine_pass_w_kernel (sweep mode)",
                          "alg_bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms, "peak_source": src},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
@@ -353,6 +404,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="grid side: 4096 (config 2) or 16384 (config 3)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

@@ -378,4 +378,32 @@ int ref_run_steps(const ismg_grid_spec* gs, const ismg_cycle_config* cs, double*
     return on_exception();
 }
 
+// Bounded CPU sample for bench.py at grids whose capped step 1 never reaches a fine
+// sweep (16384^2): `iters` outer fine iterations as solve_two_level runs them
+// (cycles.hpp:148-161: rbgs_sweep, fine_residual into the residual field,
+// anchor_mean when singular, restrict_sum), stage and fields built once, the
+// iterations alone timed. x is updated in place.
+int ref_fine_iterations(const ismg_grid_spec* gs, double* x, const double* b, long iters,
+                        double* seconds) try {
+    GridSpec g = to_grid(gs);
+    g.validate();
+    FineStage<double> st = build_fine_stage<double>(g);
+    auto bc = pressure_bc(g);
+    TileAxis ax(g.nx, g.tile, bc[0] == PressureBcKind::periodic);
+    TileAxis ay(g.ny, g.tile, bc[2] == PressureBcKind::periodic);
+    ScalarField<double> X = load(g.nx, g.ny, x), B = load(g.nx, g.ny, b), R(g.nx, g.ny), C(ax.nc, ay.nc);
+    auto t0 = std::chrono::steady_clock::now();
+    for (long k = 0; k < iters; ++k) {
+        rbgs_sweep(st, X, B);
+        fine_residual(st, X, B, &R);
+        anchor_mean(st, X);
+        restrict_sum(R, ax, ay, C);
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    store(X, x);
+    return 0;
+} catch (...) {
+    return on_exception();
+}
+
 }  // extern "C"

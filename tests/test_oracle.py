@@ -423,3 +423,24 @@ def test_port_equals_reference_random(port, ref):
             r2 = ref.solve(g, cfg, X2, bb)
             assert r1[0] == r2[0] and r1[1] == r2[1]
             assert np.array_equal(X1.data, X2.data)
+
+
+def test_bench_fine_iteration_sample(port, ref):
+    """bench.py's bounded CPU sample at 16384^2 (ref_fine_iterations in oracle/ref_shim.cpp)
+    runs the outer fine iteration of cycles.hpp:148-161: same x as the port's op loop."""
+    import ctypes as C
+    import dataclasses
+    g = dataclasses.replace(setup_lid_cavity(48, 1000.0).grid, tile=8)
+    b = random_field(48, 48, np.random.default_rng(3))
+    x_ref, x_port = ScalarField(48, 48), ScalarField(48, 48)
+    secs = C.c_double()
+    rc = ref._fn("fine_iterations")(C.byref(g.to_c()), C.c_void_p(x_ref.data.ctypes.data),
+                                    C.c_void_p(b.data.ctypes.data), C.c_long(3), C.byref(secs))
+    assert rc == 0 and secs.value >= 0.0
+    res, cb = ScalarField(48, 48), ScalarField(6, 6)
+    for _ in range(3):
+        port.rbgs_sweep(g, x_port, b)
+        port.fine_residual(g, x_port, b, res)
+        port.anchor_mean(g, x_port)
+        port.restrict_sum(g, res, cb)
+    assert np.array_equal(x_ref.data, x_port.data)
