@@ -1,9 +1,9 @@
 #!/usr/bin/env python
 """Benchmark: ISM pressure solve (arXiv 1309.7128) on B200 — fine-grid cell-updates/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 4096|16384]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--grid 4096|16384]
 
---n 16384 runs BASELINE.json configs[2] (config 3, coarse 512^2) instead of the
+--grid 16384 runs BASELINE.json configs[2] (config 3, coarse 512^2) instead of the
 default config 2; every other setting is the same.
 
 Workload (BASELINE.json configs[1]): lid-driven
@@ -198,7 +198,7 @@ def run_reference_arm(args, rank, world):
         return
     import psutil
     kind = cpu_kind()
-    n = args.n
+    n = args.grid
     ncpu = os.cpu_count() or 1
     mem_gb = psutil.virtual_memory().available / 2 ** 30
     cores = max(1, min(ncpu, int(mem_gb // 2.5)))
@@ -247,7 +247,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.current_stream()
     ctx = P.Context(local_rank, stream.cuda_stream)
-    n = args.n
+    n = args.grid
     case, cfg = workload(n)
     g = case.grid
     cells = n * n
@@ -404,7 +404,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT, help="grid side: 4096 (config 2) or 16384 (config 3)")
+    ap.add_argument("--grid", type=int, default=N_DEFAULT, help="grid side: 4096 (config 2) or 16384 (config 3)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
