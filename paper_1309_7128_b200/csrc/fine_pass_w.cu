@@ -569,6 +569,13 @@ int fine_pass_w_quads(int tile) {
     const int g = tile / 4;
     return (30 / g) * g;
 }
+int fine_pass_w_resident(bool mp, int device) {
+    int per_sm = 0, sms = 0;
+    if (mp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<true>, 32, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<false>, 32, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return std::max(1, per_sm) * std::max(1, sms);
+}
 size_t fine_pass_w_smem() { return 0; }  // static shared memory
 void set_fine_pass_w_smem() {}
 dim3 fine_pass_w_grid(const Params& P) {

@@ -296,6 +296,7 @@ size_t fine_pass_smem();
 void set_fine_pass_smem(size_t bytes);
 // independent warp strips (fine_pass_w.cu; tiles >= 4)
 int fine_pass_w_quads(int tile);
+int fine_pass_w_resident(bool mp, int device);  // resident one-warp CTAs on the device
 size_t fine_pass_w_smem();
 void set_fine_pass_w_smem();
 dim3 fine_pass_w_grid(const Params& P);

@@ -34,7 +34,7 @@ def rel_l2(a, b):
 
 
 @pytest.mark.parametrize("kernel", ["warp", "pair"])
-@pytest.mark.parametrize("rows", ["8", "16", "default"])
+@pytest.mark.parametrize("rows", ["8", "16", "64", "96", "default"])
 @pytest.mark.parametrize("nx,ny,tile", GRIDS)
 def test_fine_pass_bitwise_vs_oracle_sweeps(dev, port, monkeypatch, kernel, rows, nx, ny, tile):
     P = dev
