@@ -124,12 +124,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def fine_traffic():
+def fine_traffic(n=N_DEFAULT):
     """DRAM bytes per launch of the fine pass from the committed ncu --set full capture
     (profiles/fine_pass_traffic.json, dram__bytes_read.sum + dram__bytes_write.sum), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "fine_pass_traffic.json")) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+            return float(json.load(f)["by_grid"][str(n)]["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -398,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": bytes_io,
                     "d2h_bytes_per_step": bytes_io},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": fine_traffic() if n == 4096 else None, "kernel": "fine_pass_w_kernel (sweep mode)",
+                         "traffic": fine_traffic(n), "kernel": "fine_pass_w_kernel (sweep mode)",
                          "alg_bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms, "peak_source": src},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
