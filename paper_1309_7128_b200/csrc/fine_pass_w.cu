@@ -39,6 +39,9 @@ namespace {
 #ifndef ISMG_MP_FENCE_SC
 #define ISMG_MP_FENCE_SC 0
 #endif
+#ifndef ISMG_FINE_MINB_PR
+#define ISMG_FINE_MINB_PR 14  // the prolongation / residual kernel
+#endif
 #ifndef ISMG_FINE_MINB_MP
 #define ISMG_FINE_MINB_MP 1  // the multi-GPU variant spills at 14
 #endif
@@ -131,6 +134,11 @@ __device__ __forceinline__ void fence_release_sys() {
 #else
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 #endif
+}
+
+// a positive power of two (zero significand bits): its reciprocal is exact
+__device__ __forceinline__ bool is_pow2(double d) {
+    return d > 0.0 && (__double_as_longlong(d) & 0x000FFFFFFFFFFFFFll) == 0;
 }
 
 // this rank's own pack slot of pass parity p in its exchange buffer
@@ -549,17 +557,149 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
     warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
 }
 
+// ---- PROLONG / RESID, the split single-GPU kernel's version: the columns of a quad that
+// share a coarse pair share its row terms (same values, bit for bit). x' = x + c + P ce
+// (coarsening.hpp:495-500), residual and
+// restriction of x'. Iteration k loads (and prolongs) row k and forms the
+// residual of row k-1 with rows k-2, k-1 in registers.
 template <bool MP>
-__global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : ISMG_FINE_MINB) fine_pass_w_kernel(Params P, int nq) {
+__device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl& st, int nq, bool prolong) {
+    const int W = 4 * nq;
+    const int a = blockIdx.x * W;
+    const Lane L(P, a, nq);
+    Geo G;
+    G.r0 = P.row0 + blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.row1), G.ny = P.ny;
+    G.c = st.has_shift ? st.shift : -0.0;
+    G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
+    G.outp = st.buf[st.cur ^ 1] + L.c0;
+    G.pitch = P.pitch;
+    const int mpp = int(st.mp_seq & 1ull);  // multi-GPU: this pass's pack parity
+    double* mpk = MP ? my_pack(P, mpp) : nullptr;
+    const int tmask = P.tile - 1, lg = ilog2(P.tile);
+    const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
+    const double* xin = st.buf[st.cur];
+    const double* brow0 = st.b + (a - 4);
+    auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
+        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1) : xin + int64_t(k) * G.pitch + (a - 4);
+    };
+    Acc A;
+    // TileAxis::locate_cell of the lane's columns
+    int I0[4], I1[4];
+    double sq[4], dxq[4], idx[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        I0[q] = I1[q] = 0, sq[q] = 0.0, dxq[q] = 1.0;
+        if (prolong && L.dom[q]) {
+            const int col = L.c0 + q;
+            I0[q] = P.ax.k0[col], I1[q] = P.ax.k1[col], sq[q] = P.ax.t[col], dxq[q] = P.ax.dk[col];
+        }
+        idx[q] = is_pow2(dxq[q]) ? 1.0 / dxq[q] : 0.0;  // exact reciprocal, or 0: divide
+    }
+    // columns of a quad that share the previous column's coarse pair reuse its row terms
+    // (a quad inside one half tile: one pair, 4 coarse loads per row instead of 16)
+    bool same[4];
+    same[0] = false;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) same[q] = I0[q] == I0[q - 1] && I1[q] == I1[q - 1];
+    const int kfirst = G.r0 - 1, klast = G.r1;
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
+        issue_row_w(sm, xsrc(kfirst + s), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    double x1[4] = {0, 0, 0, 0}, x2[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
+    int slot = 0;
+    uint32_t phase = 0;
+    const int si = 4 * L.l;
+    for (int k = kfirst; k <= klast; ++k) {
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
+        double x0[4], b0[4];
+        {
+            const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
+            const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
+            const double2 c01 = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+            const double2 c23 = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+            const double raw[4] = {v01.x, v01.y, v23.x, v23.y};
+            b0[0] = c01.x, b0[1] = c01.y, b0[2] = c23.x, b0[3] = c23.y;
+            const bool rin = k >= 0 && k < G.ny;
+            double tt = 0.0, dy = 1.0;
+            int J0 = 0, J1 = 0;
+            if (prolong && rin) tt = P.ay.t[k], dy = P.ay.dk[k], J0 = P.ay.k0[k], J1 = P.ay.k1[k];
+            const double wy0 = dy - tt;
+            // power-of-two extents (uniform tiles): num / (dx dy) is exactly num ((1/dx) (1/dy))
+            const double idy = is_pow2(dy) ? 1.0 / dy : 0.0;
+            double ca = 0.0, cb = 0.0;  // the column pair's row terms (dy-t) c(I,J0) + t c(I,J1)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double v = (rin && L.dom[q]) ? raw[q] + G.c : 0.0;
+                if (prolong && rin && L.dom[q]) {
+                    if (!same[q]) {
+                        ca = wy0 * P.ce.at(I0[q], J0) + tt * P.ce.at(I0[q], J1);
+                        cb = wy0 * P.ce.at(I1[q], J0) + tt * P.ce.at(I1[q], J1);
+                    }
+                    const double num = (dxq[q] - sq[q]) * ca + sq[q] * cb;
+                    const double r = idx[q] * idy;
+                    v += r != 0.0 ? num * r : num / (dxq[q] * dy);
+                }
+                x0[q] = v;
+            }
+        }
+        const double W1 = sh_up(x1[3]), E1 = sh_dn(x1[0]);
+        const int j = k - 1;
+        if (L.owned && j >= G.r0 && j < G.r1) {
+            const double dr = row_part(G, j);
+            double r[4];
+            r[0] = b1[0] - ((((W1 + x1[1]) + x2[0]) + x0[0]) - (L.dc[0] + dr) * x1[0]);
+            r[1] = b1[1] - ((((x1[0] + x1[2]) + x2[1]) + x0[1]) - (L.dc[1] + dr) * x1[1]);
+            r[2] = b1[2] - ((((x1[1] + x1[3]) + x2[2]) + x0[2]) - (L.dc[2] + dr) * x1[2]);
+            r[3] = b1[3] - ((((x1[2] + E1) + x2[3]) + x0[3]) - (L.dc[3] + dr) * x1[3]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
+            A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
+            A.sx = A.sx + ((x1[0] + x1[1]) + (x1[2] + x1[3]));
+            A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
+            if (prolong) put_row(G, L, j, x1);
+        }
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<MP>(P, L, j, lg, A, mpk);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x2[q] = x1[q], x1[q] = x0[q], b1[q] = b0[q];
+        __syncwarp();
+        if (k + kRingW <= klast)
+            issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
+        if (++slot == kRingW) slot = 0, phase ^= 1u;
+    }
+    if (MP) mp_push(P, L, G, mpp, prolong ? G.outp : xin + L.c0);
+    warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
+}
+
+// PH selects the phases a kernel serves: 0 all, 2 the prolongation / residual pass
+// (prolong_w2). A single-GPU graph slot launches PH 2 then PH 0; the kernel whose
+// phase it is not exits at once. The PH 0 kernel is the sweep kernel, compiled as it
+// was before the split: the sweep sits at the 128-register cap and its speed
+// follows the whole kernel's register allocation (measured: a sweep-only
+// instantiation, or any growth of the inlined prolongation, ran 142-144 against
+// 125 us per 4096^2 pass).
+template <bool MP, int PH>
+__global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : (PH == 2 ? ISMG_FINE_MINB_PR : ISMG_FINE_MINB))
+    fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
 #ifdef ISMG_MP_TRACE
     if (MP && threadIdx.x == 0 && (st.phase == kFine || st.phase == kProlong || st.phase == kResid))
         atomicMin(&P.ctl->mp_t0, (unsigned long long)gtimer());
 #endif
-    if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
-    else if (st.phase == kProlong) prolong_w<MP>(sm, P, st, nq, true);
-    else if (st.phase == kResid) prolong_w<MP>(sm, P, st, nq, false);
+    if (PH == 2) {
+        if (st.phase == kProlong) prolong_w2<MP>(sm, P, st, nq, true);
+        else if (st.phase == kResid) prolong_w2<MP>(sm, P, st, nq, false);
+    } else {
+        if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
+        else if (st.phase == kProlong) prolong_w<MP>(sm, P, st, nq, true);
+        else if (st.phase == kResid) prolong_w<MP>(sm, P, st, nq, false);
+    }
 }
 
 }  // namespace
@@ -571,8 +711,8 @@ int fine_pass_w_quads(int tile) {
 }
 int fine_pass_w_resident(bool mp, int device) {
     int per_sm = 0, sms = 0;
-    if (mp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<true>, 32, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<false>, 32, 0);
+    if (mp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<true, 0>, 32, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<false, 0>, 32, 0);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return std::max(1, per_sm) * std::max(1, sms);
 }
@@ -582,9 +722,15 @@ dim3 fine_pass_w_grid(const Params& P) {
     const int W = 4 * fine_pass_w_quads(P.tile);
     return dim3((P.nx + W - 1) / W, P.nchunks);
 }
-void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st) {
-    if (P.mp) fine_pass_w_kernel<true><<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
-    else fine_pass_w_kernel<false><<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
+int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only) {
+    const int nq = fine_pass_w_quads(P.tile);
+    if (P.mp) {
+        fine_pass_w_kernel<true, 0><<<grid, 32, 0, st>>>(P, nq);
+        return 1;
+    }
+    if (!sweep_only) fine_pass_w_kernel<false, 2><<<grid, 32, 0, st>>>(P, nq);
+    fine_pass_w_kernel<false, 0><<<grid, 32, 0, st>>>(P, nq);
+    return sweep_only ? 1 : 2;
 }
 
 }  // namespace fz

@@ -20,6 +20,7 @@ struct FusedEngine {
     int* d_log = nullptr;
     std::vector<int> h_log;
     cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // 8, 16, 32, 64 slots, captured once
+    int fine_launches = 1;  // kernels per fine slot (single-GPU one-warp pass: prolongation + sweep)
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
     int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands
@@ -57,9 +58,11 @@ bool fused_supported(const Solver& s) {
     return true;
 }
 
-static void launch_fine(const FusedEngine& e, cudaStream_t st) {
-    if (e.fine_kind == 2) launch_fine_pass_w(e.P, e.grid, st);
-    else launch_fine_pass(e.P, e.grid, e.smem, st);
+// returns the kernels launched (the single-GPU one-warp pass is two kernels, by phase)
+static int launch_fine(const FusedEngine& e, cudaStream_t st, bool sweep_only = false) {
+    if (e.fine_kind == 2) return launch_fine_pass_w(e.P, e.grid, st, sweep_only);
+    launch_fine_pass(e.P, e.grid, e.smem, st);
+    return 1;
 }
 
 // multi-GPU, after every fine-pass slot: the fine pass has stored its pack into
@@ -92,7 +95,7 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
             launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
         else
             launch_coarse_global(e.P, c.stream);
-        launch_fine(e, c.stream);
+        e.fine_launches = launch_fine(e, c.stream);
         if (e.P.mp) mp_exchange(e, c);
     }
     ISMG_CUDA(cudaStreamEndCapture(c.stream, &g));
@@ -323,10 +326,9 @@ double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters) {
     for (auto& v : ev) ISMG_CUDA(cudaEventCreate(&v));
     ISMG_CUDA(cudaEventRecord(ev[0], c.stream));
     for (int k = 0; k < iters; ++k) {
-        launch_fine(e, c.stream);
+        c.launches += launch_fine(e, c.stream, true);
         ISMG_CUDA(cudaEventRecord(ev[size_t(k) + 1], c.stream));
     }
-    c.launches += iters;
     ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     double total = 0.0;
@@ -383,7 +385,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     int since_poll = 0;
     for (;;) {
         ISMG_CUDA(cudaGraphLaunch(graph_for(e, slots), c.stream));
-        c.launches += (e.P.mp ? 3 : 2) * slots + (e.cl_hybrid ? slots : 0);
+        c.launches += (1 + e.fine_launches + (e.P.mp ? 1 : 0)) * slots + (e.cl_hybrid ? slots : 0);
         launched_slots += slots;
         ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
         ISMG_CUDA(cudaEventRecord(e.ev, c.stream));

@@ -300,7 +300,8 @@ int fine_pass_w_resident(bool mp, int device);  // resident one-warp CTAs on the
 size_t fine_pass_w_smem();
 void set_fine_pass_w_smem();
 dim3 fine_pass_w_grid(const Params& P);
-void launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st);
+// kernels launched: single-GPU, the prolongation kernel then the sweep kernel (sweep_only: the sweep)
+int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only = false);
 void launch_finalize(const Params& P, View xuser, cudaStream_t st);
 void launch_mp_unpack(const Params& P, cudaStream_t st);
 void launch_coarse_global(const Params& P, cudaStream_t st);
