@@ -54,17 +54,44 @@ TILE = 32
 REF_SAMPLE_CAP = 3000  # max_total_sweeps of the bounded CPU sample (step 1)
 
 
-def config_name(n):
+JET_NX = 8192  # config 4: jet 8192 x 16384
+
+
+def config_name(n, kind="lid"):
+    if kind == "jet":
+        return "config 4" if n == JET_NX else "jet %dx%d" % (n, 2 * n)
     return "config 3" if n == 16384 else ("config 2" if n == 4096 else "lid %d^2" % n)
 
 
-def workload(n=N_DEFAULT):
-    from paper_1309_7128_b200.api import CycleConfig, setup_lid_cavity
-    case = setup_lid_cavity(n, RE)
-    case.dt = RE / n  # dt = Re/n: the reference default dt = 1 diverges
+def workload(n=N_DEFAULT, kind="lid"):
+    """The bench workloads. lid: config 2 / 3, lid cavity n x n, Re 1000,
+    tile 32. jet: config 4, setup_jet(n, 2n, 0.1, 16) (bench.hpp:73-88), dt 1, tile 16
+    (jet.cfg:15): non-singular (fixed-pressure top), so no anchoring."""
+    from paper_1309_7128_b200.api import CycleConfig, setup_jet, setup_lid_cavity
+    if kind == "jet":
+        case = setup_jet(n, 2 * n, 0.1, 16)
+        tile = 16
+    else:
+        case = setup_lid_cavity(n, RE)
+        case.dt = RE / n  # dt = Re/n: the reference default dt = 1 diverges (SURVEY.md §0.2)
+        tile = TILE
     case.steps, case.t_max, case.steady_tol = 10 ** 9, 0.0, 0.0
-    cfg = CycleConfig(tile=TILE, tol_fine=1e-6, tol_coarse=1e-5, max_total_sweeps=20000, stall_factor=0.9)
+    cfg = CycleConfig(tile=tile, tol_fine=1e-6, tol_coarse=1e-5, max_total_sweeps=20000, stall_factor=0.9)
     return case, cfg
+
+
+def grid_side(args):
+    """nx of the workload: --grid for the lid; for the jet 8192 (config 4) unless --grid is given."""
+    if args.case == "jet" and args.grid == N_DEFAULT:
+        return JET_NX
+    return args.grid
+
+
+def workload_desc(n, kind):
+    if kind == "jet":
+        return "turbulent jet %dx%d, v0 0.1, inlet 16, nu 0.01, dt 1, ISM 16h two-level (%s)" % (
+            n, 2 * n, config_name(n, kind))
+    return "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (%s)" % (n, n, config_name(n))
 
 
 def peaks():
@@ -134,11 +161,11 @@ def fine_traffic(n=N_DEFAULT):
         return None
 
 
-def cpu_sample(kind, n=N_DEFAULT, cap=REF_SAMPLE_CAP):
+def cpu_sample(kind, n=N_DEFAULT, cap=REF_SAMPLE_CAP, case_kind="lid"):
     """One bounded reference sample: step 1 with the sweep budget capped. Returns (I_f, seconds)."""
     from pyoracle import Oracle
     from paper_1309_7128_b200.api import FluidState
-    case, cfg = workload(n)
+    case, cfg = workload(n, case_kind)
     cfg.max_total_sweeps = cap
     st = FluidState(case.grid)
     st.dt, st.nu = case.dt, case.nu
@@ -154,35 +181,35 @@ def cpu_kind():
     return "reference" if available("reference") else "port"
 
 
-def cpu_fine_iterations(kind, n, iters):
+def cpu_fine_iterations(kind, n, iters, case_kind="lid"):
     """Bounded reference sample for grids whose capped step 1 never reaches a fine sweep:
     `iters` outer fine iterations of step 1 (cycles.hpp:148-161: rbgs_sweep, fine_residual
     into the residual field, anchor_mean, restrict_sum) on the step-1 rhs, timed on one core.
     Returns (fine sweeps, seconds)."""
     from pyoracle import Oracle
     from paper_1309_7128_b200.api import FluidState, MacVelocity, ScalarField
-    case, cfg = workload(n)
+    case, cfg = workload(n, case_kind)
     g = case.grid
+    nx, ny = g.nx, g.ny
     o = Oracle(kind)
     st = FluidState(g)
     o.apply_velocity_bc(g, st.vel)
-    vstar = MacVelocity(n, n)
+    vstar = MacVelocity(nx, ny)
     o.predictor(g, st.vel, st.p, case.dt, case.nu, vstar)
     o.apply_velocity_bc(g, vstar)
-    b = ScalarField(n, n)
+    b = ScalarField(nx, ny)
     o.divergence(g, vstar, b)
     b.data *= g.h * g.h / case.dt
     gt = dataclasses.replace(g, tile=cfg.tile)  # restrict_sum tiles the grid by the cycle's tile
-    x = ScalarField(n, n)
+    x = ScalarField(nx, ny)
     if kind == "reference":  # stage and fields built once inside the reference, iterations timed there
         import ctypes as C
         secs = C.c_double()
         o._check(o._fn("fine_iterations")(C.byref(gt.to_c()), C.c_void_p(x.data.ctypes.data),
                                           C.c_void_p(b.data.ctypes.data), C.c_long(iters), C.byref(secs)))
         return iters, secs.value
-    res = ScalarField(n, n)
-    nc = (n + cfg.tile - 1) // cfg.tile
-    cb = ScalarField(nc, nc)
+    res = ScalarField(nx, ny)
+    cb = ScalarField((nx + cfg.tile - 1) // cfg.tile, (ny + cfg.tile - 1) // cfg.tile)
     t0 = time.perf_counter()
     for _ in range(iters):
         o.rbgs_sweep(gt, x, b)
@@ -198,18 +225,19 @@ def run_reference_arm(args, rank, world):
         return
     import psutil
     kind = cpu_kind()
-    n = args.grid
+    ck = args.case
+    n = grid_side(args)
     ncpu = os.cpu_count() or 1
     mem_gb = psutil.virtual_memory().available / 2 ** 30
-    cells = n * n
+    cells = n * n * (2 if ck == "jet" else 1)
     cores = max(1, min(ncpu, int(mem_gb // (2.5 * cells / 4096 ** 2))))
-    small = n == N_DEFAULT  # else a capped step 1 never reaches a fine sweep: sample fine iterations
+    small = n == N_DEFAULT and ck == "lid"  # else a capped step 1 never reaches a fine sweep: sample fine iterations
 
     def round_(cap):
         res = [None] * cores
 
         def work(k):
-            res[k] = cpu_sample(kind, n, cap) if small else cpu_fine_iterations(kind, n, 1 if cap < 1000 else 2)
+            res[k] = cpu_sample(kind, n, cap, ck) if small else cpu_fine_iterations(kind, n, 1 if cap < 1000 else 2, ck)
         th = [threading.Thread(target=work, args=(k,)) for k in range(cores)]
         t0 = time.perf_counter()
         for t in th:
@@ -233,14 +261,15 @@ def run_reference_arm(args, rank, world):
         tot_t += t
     value = tot_if * cells / tot_t
     what = ("step 1 of lid %d^2 Re 1000 (dt = Re/n, tile 32) capped at %d sweeps" % (n, REF_SAMPLE_CAP) if small else
-            "2 outer fine iterations of step 1 of lid %d^2 (rbgs_sweep, fine_residual, anchor_mean, restrict_sum)" % n)
+            "2 outer fine iterations of step 1 of %s (rbgs_sweep, fine_residual, anchor_mean, restrict_sum)"
+            % workload_desc(n, ck))
     sample = ("%s, %d independent single-threaded solves in parallel (the reference solve has no intra-solve "
               "threading)" % (what, cores))
     line = {
         "impl": "reference", "metric": "fine-grid cell-updates/s", "value": value, "unit": "cell-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "lid-driven cavity %dx%d Re=1000, ISM 32h two-level (%s)" % (n, n, config_name(n)),
+        "config": {"workload": workload_desc(n, ck),
                    "global_batch": 1, "seq_len": 0, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -256,10 +285,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.current_stream()
     ctx = P.Context(local_rank, stream.cuda_stream)
-    n = args.grid
-    case, cfg = workload(n)
+    ck = args.case
+    n = grid_side(args)
+    case, cfg = workload(n, ck)
     g = case.grid
-    cells = n * n
+    nx, ny = g.nx, g.ny
+    cells = nx * ny
     dist = world > 1
     if dist:  # strip decomposition: one NCCL communicator over the ranks
         import torch.distributed as tdist
@@ -352,12 +383,12 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         ctx = P.Context(local_rank, stream.cuda_stream)
         solver = P.PressureSolver(g, cfg, ctx)
-    xs = P.DeviceField(n, n, ctx)
-    bs = P.DeviceField(n, n, ctx)
+    xs = P.DeviceField(nx, ny, ctx)
+    bs = P.DeviceField(nx, ny, ctx)
     # rhs of the timed run's first step, rebuilt through the public kernels
-    vel = P.DeviceVelocity(n, n, ctx)
-    vstar = P.DeviceVelocity(n, n, ctx)
-    pf = P.DeviceField(n, n, ctx)
+    vel = P.DeviceVelocity(nx, ny, ctx)
+    vstar = P.DeviceVelocity(nx, ny, ctx)
+    pf = P.DeviceField(nx, ny, ctx)
     P.apply_velocity_bc(vel, g)
     vstar.upload(vel.download())
     P.predictor(vel, pf, case.dt, case.nu, g, vstar)
@@ -371,11 +402,11 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         kind = cpu_kind()
-        if n == N_DEFAULT:
+        if n == N_DEFAULT and ck == "lid":
             i_f, secs = cpu_sample(kind, n)
             smp = "step 1 of the same workload capped at %d sweeps (I_f %d in %.1f s)" % (REF_SAMPLE_CAP, i_f, secs)
         else:  # a capped step 1 at 16384^2 spends its whole budget in the first coarse visit
-            i_f, secs = cpu_fine_iterations(kind, n, 2)
+            i_f, secs = cpu_fine_iterations(kind, n, 2, ck)
             smp = ("%d outer fine iterations of step 1 (rbgs_sweep, fine_residual, anchor_mean, restrict_sum) "
                    "in %.1f s" % (i_f, secs))
         cpu = {"value": i_f * cells / secs, "unit": "cell-updates/s", "cores": 1, "kind": kind, "sample": smp}
@@ -385,20 +416,20 @@ def run_ours(args, rank, world, local_rank):
             "metric": "fine-grid cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (quiescent lid-driven cavity, seed 0)",
-            "config": {"workload": "lid-driven cavity %dx%d Re=1000, dt=Re/n, ISM 32h two-level (%s)" % (n, n, config_name(n)),
+            "data": "synthetic (quiescent %s, seed 0)" % ("jet box" if ck == "jet" else "lid-driven cavity"),
+            "config": {"workload": workload_desc(n, ck),
                        "global_batch": 1, "seq_len": 0,
                        "parallelism": ("y-strips x%d (halo rows pushed over NVLink by the fine pass, partials "
                                        "and coarse-rhs rows pulled from peer memory; coarse solve replicated)"
                                        % world) if dist else "single GPU",
                        "steps_timed": "projection steps 1..%d" % args.steps,
-                       "l2": "inputs larger than L2 (x, scratch, b: 3 x %.0f MB vs 126 MB L2)" % (8.0 * (n + 2) ** 2 / 1e6),
+                       "l2": "inputs larger than L2 (x, scratch, b: 3 x %.0f MB vs 126 MB L2)" % (8.0 * (nx + 2) * (ny + 2) / 1e6),
                        "fine_sweeps": int(fine_all), "coarse_sweeps": int(coarse)},
             "pressure_solves_per_s": args.steps / (ms_max * 1e-3),
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": bytes_io,
                     "d2h_bytes_per_step": bytes_io},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": fine_traffic(n), "kernel": "fine_pass_w_kernel (sweep mode)",
+                         "traffic": fine_traffic(n if ck == "lid" else "jet%d" % n), "kernel": "fine_pass_w_kernel (sweep mode)",
                          "alg_bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms, "peak_source": src},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
@@ -414,6 +445,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--grid", type=int, default=N_DEFAULT, help="grid side: 4096 (config 2) or 16384 (config 3)")
+    ap.add_argument("--case", default="lid", choices=["lid", "jet"],
+                    help="lid: lid cavity --grid^2 (configs 2, 3); jet: config 4, jet nx x 2nx (nx = 8192 unless --grid)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
