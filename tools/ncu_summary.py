@@ -26,18 +26,21 @@ def ncu(path, *args):
 
 def main(path):
     rows = list(csv.reader(io.StringIO(ncu(path, "--page", "raw", "--csv"))))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u = rows[0], rows[1]
     print("# ncu --set full summary of %s" % path.split("/")[-1])
-    for k in KEYS:
-        if k in h:
-            print("%-62s %s %s" % (k, v[h.index(k)], u[h.index(k)]))
+    for n, v in enumerate(rows[2:]):  # one block per captured launch
+        print("\n## launch %d" % n)
+        for k in KEYS:
+            if k in h:
+                print("%-62s %s %s" % (k, v[h.index(k)], u[h.index(k)]))
+    # source page: the first captured launch
     src = list(csv.reader(io.StringIO(ncu(path, "--page", "source", "--csv", "--print-source", "sass"))))
     sh, sd = src[1], src[2:]
     idx = {n: sh.index(n) for n in STALLS if n in sh}
     agg = collections.Counter()
     for r in sd:
         for n, i in idx.items():
-            if r[i].isdigit():
+            if i < len(r) and r[i].isdigit():
                 agg[n] += int(r[i])
     tot = sum(agg.values()) or 1
     print("\nwarp stall samples (share):")
@@ -46,6 +49,7 @@ def main(path):
             print("  %-24s %6d  %5.1f%%" % (n, c, 100.0 * c / tot))
     iS, iE, iW = sh.index("Source"), sh.index("Instructions Executed"), sh.index("Warp Stall Sampling (All Samples)")
     print("\ntop SASS lines by stall samples (executed, samples, instruction):")
+    sd = [r for r in sd if len(r) > max(iS, iE, iW)]
     for r in sorted(sd, key=lambda r: -int(r[iW]) if r[iW].isdigit() else 0)[:15]:
         print("  %10s %6s  %s" % (r[iE], r[iW], r[iS].strip()[:90]))
 
