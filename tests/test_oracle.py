@@ -444,3 +444,16 @@ def test_bench_fine_iteration_sample(port, ref):
         port.anchor_mean(g, x_port)
         port.restrict_sum(g, res, cb)
     assert np.array_equal(x_ref.data, x_port.data)
+
+
+def test_bench_jet_workload_and_sample(port, ref):
+    """bench.py --case jet (config 4): setup_jet(n, 2n, 0.1, 16) (bench.hpp:73-88), tile 16
+    (jet.cfg:15); the bounded fine-iteration sample runs on the nx x 2nx grid and the
+    reference and the port land on the same fine sweep count."""
+    import bench
+    case, cfg = bench.workload(bench.JET_NX, "jet")
+    assert (case.grid.nx, case.grid.ny, cfg.tile) == (8192, 16384, 16)
+    assert "config 4" in bench.workload_desc(bench.JET_NX, "jet")
+    for kind in ("reference", "port"):
+        i_f, secs = bench.cpu_fine_iterations(kind, 32, 2, "jet")
+        assert i_f == 2 and secs >= 0.0
