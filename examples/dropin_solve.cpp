@@ -30,10 +30,8 @@ int main() {
     ismg_b200::Context ctx(0);
     ismg_b200::PressureSolver solver(grid, cfg, ctx);  // B200
     for (int k = 0; k < 5; ++k) {
-        const auto rep = ismg_b200::step(st, grid, solver, m, ctx);
-        m.close_timestep(st.step_count, rep.residual, rep.converged);
+        const auto rep = ismg_b200::step(st, grid, solver, m);  // same call as the reference's
         const auto rr = ismg::step(ref, grid, ref_solver, mr);
-        mr.close_timestep(ref.step_count, rr.residual, rr.converged);
         std::printf("step %d: B200 I_f %ld I_c %ld | reference I_f %ld I_c %ld\n", k + 1, rep.fine_sweeps,
                     rep.coarse_sweeps, rr.fine_sweeps, rr.coarse_sweeps);
     }
@@ -42,6 +40,11 @@ int main() {
         const double d = st.p.data[i] - ref.p.data[i];
         num += d * d, den += ref.p.data[i] * ref.p.data[i];
     }
-    std::printf("pressure rel L2 %.3e\n", den > 0 ? std::sqrt(num / den) : std::sqrt(num));
-    return 0;
+    const double err = den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+    bool same = m.rows.size() == mr.rows.size();
+    for (size_t k = 0; same && k < m.rows.size(); ++k)
+        same = m.rows[k].fine_sweeps == mr.rows[k].fine_sweeps && m.rows[k].coarse_sweeps == mr.rows[k].coarse_sweeps &&
+               m.rows[k].restrictions == mr.rows[k].restrictions && m.rows[k].step == mr.rows[k].step;
+    std::printf("pressure rel L2 %.3e, metrics rows %s\n", err, same ? "identical" : "DIFFER");
+    return (same && err <= 1e-10) ? 0 : 1;
 }

@@ -41,7 +41,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define ISMG_B200_ABI_VERSION 1
+#define ISMG_B200_ABI_VERSION 2
 
 /* ---- status codes -------------------------------------------------------- */
 enum {
@@ -147,6 +147,9 @@ typedef struct ismg_solve_stats {
     double coarse_ms;           /* summed CUDA-event time of coarse visits    */
     double solve_ms;            /* CUDA-event time of the whole solve         */
     int64_t coarse_steps;       /* wavefront steps of the coarse visits       */
+    int64_t coarse_engine;      /* coarse-visit kernel of the fused path: 0 global
+                                   wavefront, 1 shared-memory iterate, 2 TMEM rhs,
+                                   3 cluster bands, 4 register wavefront; -1 op-level */
 } ismg_solve_stats;
 
 /* ---- opaque handles ------------------------------------------------------ */
@@ -265,6 +268,16 @@ int ismg_solver_visit_log(const ismg_solver* s, int32_t* out, size_t cap, size_t
  * non-periodic, power-of-two tile <= 64). x is relaxed in place. */
 int ismg_bench_fine_pass(ismg_solver* s, ismg_field* x, const ismg_field* b, int iters,
                          double* ms_per_pass);
+/* Measurement / parity hook (no reference counterpart): ONE coarse visit
+ * (cycles.hpp:120-137: gs_sweep_lex + coarse_residual until tol_coarse, then
+ * the coarse anchor when singular) of the fused path's coarse-visit kernel on
+ * rhs cb (coarse extent ncx x ncy), from ce = 0, with at most `budget` sweeps;
+ * the first sweep group holds `first_group` sweeps (the visit-length
+ * prediction). ce receives the iterate, *sweeps the sweeps run, *rc the final
+ * coarse residual max, *ms the kernel's CUDA-event time. Requires the fused
+ * path. */
+int ismg_bench_coarse_visit(ismg_solver* s, const ismg_field* cb, ismg_field* ce, int64_t budget, int first_group,
+                            int64_t* sweeps, double* rc, double* ms);
 /* kernels launched through this context so far (stream order) */
 int ismg_ctx_launch_count(const ismg_ctx* ctx, int64_t* out);
 

@@ -120,11 +120,12 @@ class Context {
 };
 
 // PressureSolver — cycles.hpp:286-333. Builds the operator once (host) and
-// keeps it on the device; solve() is const like the reference's.
+// keeps it on the device; solve() is const like the reference's. The solver
+// remembers its context, so step() takes the reference's four arguments.
 class PressureSolver {
   public:
     template <class Grid, class Cfg>
-    PressureSolver(const Grid& grid, const Cfg& cfg, Context& ctx) : nx_(grid.nx), ny_(grid.ny) {
+    PressureSolver(const Grid& grid, const Cfg& cfg, Context& ctx) : ctx_(&ctx), nx_(grid.nx), ny_(grid.ny) {
         const ismg_grid_spec g = grid_to_c(grid);
         const ismg_cycle_config c = cycle_to_c(cfg);
         check(ismg_solver_create(ctx.get(), &g, &c, &h_));
@@ -148,38 +149,77 @@ class PressureSolver {
     }
 
     ismg_solver* get() const { return h_; }
+    Context& context() const { return *ctx_; }
     int nx() const { return nx_; }
     int ny() const { return ny_; }
 
   private:
+    Context* ctx_;
     ismg_solver* h_ = nullptr;
     int nx_, ny_;
 };
 
-// step — projection.hpp:139-190, on a host FluidState<double>: the state is
-// uploaded, advanced one projection step on the device, and downloaded.
+// FluidState<double> resident in HBM across steps (no per-step upload /
+// download): upload once, step many times, download when needed.
+class DeviceState {
+  public:
+    template <class Grid>
+    DeviceState(const Grid& grid, Context& ctx) {
+        const ismg_grid_spec g = grid_to_c(grid);
+        check(ismg_state_create(ctx.get(), &g, &h_));
+    }
+    ~DeviceState() {
+        if (h_) ismg_state_destroy(h_);
+    }
+    DeviceState(const DeviceState&) = delete;
+    DeviceState& operator=(const DeviceState&) = delete;
+
+    template <class State>
+    void upload(const State& st) {
+        check(ismg_state_set_scalars(h_, st.t, st.dt, st.nu, int64_t(st.step_count)));
+        check(ismg_state_upload(h_, st.vel.u_data.data(), st.vel.u_data.size(), st.vel.v_data.data(),
+                                st.vel.v_data.size(), st.p.data.data(), st.p.data.size()));
+    }
+    template <class State>
+    void download(State& st) const {
+        check(ismg_state_download(h_, st.vel.u_data.data(), st.vel.u_data.size(), st.vel.v_data.data(),
+                                  st.vel.v_data.size(), st.p.data.data(), st.p.data.size()));
+        int64_t steps = 0;
+        check(ismg_state_get_scalars(h_, &st.t, &st.dt, &st.nu, &steps));
+        st.step_count = decltype(st.step_count)(steps);
+    }
+    // projection.hpp:139-190 on the resident state; closes the metrics row like
+    // the reference (m.close_timestep, with (0, true) for dt == 0, :163-165)
+    template <class Metrics>
+    ConvergenceReport step(const PressureSolver& solver, Metrics& m) {
+        ismg_report r{};
+        ismg_step_metrics cur = metrics_in(m);
+        check(ismg_step(h_, solver.get(), &r, &cur, m.fine_cells));
+        metrics_out(m, cur);
+        double t = 0, dt = 0, nu = 0;
+        int64_t steps = 0;
+        check(ismg_state_get_scalars(h_, &t, &dt, &nu, &steps));
+        const ConvergenceReport rep = report(r);
+        m.close_timestep(long(steps), dt == 0.0 ? 0.0 : rep.residual, dt == 0.0 ? true : rep.converged);
+        return rep;
+    }
+    ismg_state* get() const { return h_; }
+
+  private:
+    ismg_state* h_ = nullptr;
+};
+
+// step — projection.hpp:139-190 with the reference's signature, on a host
+// FluidState<double>: the state is uploaded, advanced one projection step on
+// the device (the solver's context) and downloaded; the metrics row is closed
+// as the reference closes it. For many steps keep a DeviceState instead.
 template <class State, class Grid, class Metrics>
-ConvergenceReport step(State& st, const Grid& grid, const PressureSolver& solver, Metrics& m, Context& ctx) {
-    const ismg_grid_spec g = grid_to_c(grid);
-    ismg_state* s = nullptr;
-    check(ismg_state_create(ctx.get(), &g, &s));
-    struct Guard {
-        ismg_state* s;
-        ~Guard() { ismg_state_destroy(s); }
-    } guard{s};
-    check(ismg_state_set_scalars(s, st.t, st.dt, st.nu, int64_t(st.step_count)));
-    check(ismg_state_upload(s, st.vel.u_data.data(), st.vel.u_data.size(), st.vel.v_data.data(),
-                            st.vel.v_data.size(), st.p.data.data(), st.p.data.size()));
-    ismg_report r{};
-    ismg_step_metrics cur = metrics_in(m);
-    check(ismg_step(s, solver.get(), &r, &cur, m.fine_cells));
-    metrics_out(m, cur);
-    check(ismg_state_download(s, st.vel.u_data.data(), st.vel.u_data.size(), st.vel.v_data.data(),
-                              st.vel.v_data.size(), st.p.data.data(), st.p.data.size()));
-    int64_t steps = 0;
-    check(ismg_state_get_scalars(s, &st.t, &st.dt, &st.nu, &steps));
-    st.step_count = decltype(st.step_count)(steps);
-    return report(r);
+ConvergenceReport step(State& st, const Grid& grid, const PressureSolver& solver, Metrics& m) {
+    DeviceState ds(grid, solver.context());
+    ds.upload(st);
+    const ConvergenceReport rep = ds.step(solver, m);
+    ds.download(st);
+    return rep;
 }
 
 }  // namespace ismg_b200

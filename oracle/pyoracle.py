@@ -171,6 +171,19 @@ class Oracle:
         self._fn("predictor")(C.byref(gc), dptr(vel.u_data), dptr(vel.v_data), dptr(p.data), C.c_double(dt),
                               C.c_double(nu), dptr(out.u_data), dptr(out.v_data))
 
+    def op_costs(self, g: GridSpec, cfg: CycleConfig, dt: float, nu: float, reps: int = 1):
+        """Reference only (ref_op_costs, oracle/ref_shim.cpp): seconds per call of
+        rbgs_sweep, fine_residual(+store), anchor_mean, restrict_sum,
+        prolongate_bilinear, gs_sweep_lex, coarse_residual, coarse anchor_mean,
+        and one step() from rest with a 1-sweep budget (the per-step fixed cost)."""
+        if self.kind == "port":
+            raise OracleError(-1, "op_costs: reference library only")
+        gc, cc = g.to_c(), cfg.to_c()
+        out = np.zeros(9)
+        self._check(self._fn("op_costs")(C.byref(gc), C.byref(cc), C.c_double(dt), C.c_double(nu), C.c_int(reps),
+                                         dptr(out)))
+        return out
+
     def run_steps(self, g: GridSpec, cfg: CycleConfig, state, nsteps: int):
         """run_case with seed 0 / no steady exit: returns (rows, seconds|None); state updated in place."""
         gc, cc = g.to_c(), cfg.to_c()

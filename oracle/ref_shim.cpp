@@ -1,7 +1,7 @@
 // ref_shim.cpp — C entry points onto the UNMODIFIED reference library
 // (TEST INFRASTRUCTURE ONLY).
 //
-// Compiled by oracle/build_ref.sh against the reference's own headers where
+// Compiled by oracle/build.sh against the reference's own headers where
 // they lie (-I $REF/proj/include, never copied into this repo) with the
 // reference's flags (proj/CMakeLists.txt:14: -O3, no -march => no FMA), into
 // oracle/_ref/libismg_ref.so. Used to pin the C restatement (ismg_oracle.c)
@@ -401,6 +401,111 @@ int ref_fine_iterations(const ismg_grid_spec* gs, double* x, const double* b, lo
     }
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     store(X, x);
+    return 0;
+} catch (...) {
+    return on_exception();
+}
+
+// The reference's own writers (io.hpp:35-117) on the given state: field CSV of
+// p, VTK of (p, velocity), and the ISMG operator dump of grid gs (its tile).
+int ref_write_outputs(const ismg_grid_spec* gs, const double* u, const double* v, const double* p,
+                      const char* field_csv, const char* vtk, const char* op_csv) try {
+    GridSpec g = to_grid(gs);
+    g.validate();
+    ScalarField<double> P = load(g.nx, g.ny, p);
+    MacVelocity<double> vel = load_vel(g.nx, g.ny, u, v);
+    write_field_csv(P, g, field_csv);
+    write_vtk(P, vel, g, vtk);
+    write_operator_csv(build_ismg_operator<double>(g), std::string(op_csv));
+    return 0;
+} catch (...) {
+    return on_exception();
+}
+
+// Per-operation wall cost of the reference on grid gs with cycle cs (bench.py's
+// CPU arms: the reference's own functions on this host, multiplied by a GPU
+// run's exact counts). Seconds per call, the minimum over `reps` calls, on the
+// step-1 state from rest (predictor, divergence, rhs scale as step(),
+// projection.hpp:166-178):
+//   out[0] rbgs_sweep            smoother.hpp:101-117
+//   out[1] fine_residual + store  smoother.hpp:121-141
+//   out[2] anchor_mean           smoother.hpp:145-148
+//   out[3] restrict_sum          coarsening.hpp:471-480
+//   out[4] prolongate_bilinear   coarsening.hpp:485-503
+//   out[5] gs_sweep_lex          coarsening.hpp:552-567
+//   out[6] coarse_residual       coarsening.hpp:531-549
+//   out[7] anchor_mean (coarse)  coarsening.hpp:592-595
+//   out[8] step() from rest with max_total_sweeps = 1: the per-step fixed
+//          cost (BCs, CFL scan, copies, predictor, divergence, solve set-up with
+//          its initial residual, one restriction, one coarse sweep, correction)
+int ref_op_costs(const ismg_grid_spec* gs, const ismg_cycle_config* cs, double dt, double nu, int reps,
+                 double* out) try {
+    GridSpec g = to_grid(gs);
+    CycleConfig cfg = to_cfg(cs);
+    g.tile = cfg.tile;
+    g.validate();
+    using clk = std::chrono::steady_clock;
+    auto timed = [&](auto&& fn) {
+        double best = 1e300;
+        for (int r = 0; r < std::max(1, reps); ++r) {
+            auto t0 = clk::now();
+            fn();
+            best = std::min(best, std::chrono::duration<double>(clk::now() - t0).count());
+        }
+        return best;
+    };
+    {  // out[8]: one projection step from rest, budget 1
+        CycleConfig c1 = cfg;
+        c1.max_total_sweeps = 1;
+        PressureSolver<double> solver(g, c1);
+        FluidState<double> st(g);
+        st.dt = dt, st.nu = nu;
+        RunMetrics m(std::int64_t(g.nx) * g.ny);
+        auto t0 = clk::now();
+        step(st, g, solver, m);
+        out[8] = std::chrono::duration<double>(clk::now() - t0).count();
+    }
+    FluidState<double> st(g);
+    st.dt = dt, st.nu = nu;
+    apply_scalar_bc(st.p, pressure_bc(g));
+    apply_velocity_bc(st.vel, g);
+    MacVelocity<double> vstar = st.vel;
+    predictor(st, g, vstar);
+    apply_velocity_bc(vstar, g);
+    ScalarField<double> b(g.nx, g.ny), x(g.nx, g.ny), res(g.nx, g.ny);
+    divergence(vstar, g, b);
+    const double scale = g.h * g.h / dt;
+    for (int j = 0; j < g.ny; ++j) {
+        double* r = b.row(j);
+        for (int i = 0; i < g.nx; ++i) r[i] *= scale;
+    }
+    volatile double sink = 0.0;  // keeps the residual maxima observable
+    FineStage<double> stage = build_fine_stage<double>(g);
+    CoarseOperator<double> op = build_ismg_operator<double>(g);
+    auto bc = pressure_bc(g);
+    TileAxis ax(g.nx, g.tile, bc[0] == PressureBcKind::periodic);
+    TileAxis ay(g.ny, g.tile, bc[2] == PressureBcKind::periodic);
+    ScalarField<double> cb(ax.nc, ay.nc), ce(ax.nc, ay.nc), cr(ax.nc, ay.nc);
+    out[0] = timed([&] { rbgs_sweep(stage, x, b); });
+    out[1] = timed([&] { sink = sink + fine_residual(stage, x, b, &res); });
+    out[2] = timed([&] { anchor_mean(stage, x); });
+    out[3] = timed([&] { restrict_sum(res, ax, ay, cb); });
+    int creps = std::max(1, reps) * 8;
+    double best5 = 1e300, best6 = 1e300, best7 = 1e300;
+    for (int r = 0; r < creps; ++r) {
+        auto t0 = clk::now();
+        gs_sweep_lex(op, ce, cb);
+        auto t1 = clk::now();
+        sink = sink + coarse_residual(op, ce, cb);
+        auto t2 = clk::now();
+        anchor_mean(op, ce);
+        auto t3 = clk::now();
+        best5 = std::min(best5, std::chrono::duration<double>(t1 - t0).count());
+        best6 = std::min(best6, std::chrono::duration<double>(t2 - t1).count());
+        best7 = std::min(best7, std::chrono::duration<double>(t3 - t2).count());
+    }
+    out[5] = best5, out[6] = best6, out[7] = best7;
+    out[4] = timed([&] { prolongate_bilinear(ce, ax, ay, x); });
     return 0;
 } catch (...) {
     return on_exception();

@@ -104,6 +104,7 @@ class CSolveStats(C.Structure):
         ("coarse_ms", C.c_double),
         ("solve_ms", C.c_double),
         ("coarse_steps", C.c_int64),
+        ("coarse_engine", C.c_int64),
     ]
 
 

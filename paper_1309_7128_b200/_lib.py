@@ -85,6 +85,7 @@ SIGNATURES = {
     "ismg_solver_last_stats": [VP, C.POINTER(CSolveStats)],
     "ismg_solver_visit_log": [VP, I32P, C.c_size_t, C.POINTER(C.c_size_t)],
     "ismg_bench_fine_pass": [VP, VP, VP, C.c_int, DP],
+    "ismg_bench_coarse_visit": [VP, VP, VP, C.c_int64, C.c_int, C.POINTER(C.c_int64), DP, DP],
     "ismg_ctx_launch_count": [VP, C.POINTER(C.c_int64)],
     "ismg_apply_scalar_bc": [VP, G, VP],
     "ismg_apply_velocity_bc": [VP, G, VP],

@@ -490,6 +490,67 @@ def write_summary(m: RunMetrics, window: int, os: io.TextIOBase | None = None) -
 
 
 # --------------------------------------------------------------------------
+# io.hpp: snapshot and diagnostic output (same formats as the reference)
+
+
+def _open(path):
+    try:
+        return open(path, "w", newline="\n")
+    except OSError as e:
+        raise RuntimeError("io: cannot open '%s' for writing" % path) from e
+
+
+def write_field_csv(f: "ScalarField", g: "GridSpec", path: str) -> None:
+    """io.hpp:35-50: header `nx,ny,h`, its values, then one row of interior
+    values per grid row (south to north), `%.10g`."""
+    with _open(path) as os_:
+        os_.write("nx,ny,h\n%d,%d,%s\n" % (g.nx, g.ny, _g10(g.h)))
+        a = f.interior()
+        for j in range(g.ny):
+            os_.write(",".join(_g10(float(v)) for v in a[j]) + "\n")
+
+
+def write_vtk(p: "ScalarField", vel: "MacVelocity", g: "GridSpec", path: str) -> None:
+    """io.hpp:54-94: legacy ASCII VTK structured points over cell centres, the
+    pressure and the face-averaged velocity."""
+    with _open(path) as os_:
+        w = os_.write
+        w("# vtk DataFile Version 3.0\nismg snapshot\nASCII\nDATASET STRUCTURED_POINTS\n")
+        w("DIMENSIONS %d %d 1\n" % (g.nx, g.ny))
+        w("ORIGIN %s %s 0\n" % (_g10(0.5 * g.h), _g10(0.5 * g.h)))
+        w("SPACING %s %s 1\n" % (_g10(g.h), _g10(g.h)))
+        w("POINT_DATA %d\nSCALARS pressure double 1\nLOOKUP_TABLE default\n" % (g.nx * g.ny))
+        a = p.interior()
+        for j in range(g.ny):
+            w("".join(_g10(float(v)) + "\n" for v in a[j]))
+        w("VECTORS velocity double\n")
+        U, V = vel.u_grid, vel.v_grid
+        for j in range(g.ny):
+            for i in range(g.nx):
+                uc = 0.5 * (float(U[j + 1, i + 1]) + float(U[j + 1, i + 2]))
+                vc = 0.5 * (float(V[j + 1, i + 1]) + float(V[j + 2, i + 1]))
+                w("%s %s 0\n" % (_g10(uc), _g10(vc)))
+
+
+def write_operator_csv(ncx: int, ncy: int, w, path_or_stream) -> str:
+    """io.hpp:97-117: per-cell stencil rows `ci,cj,C,E,W,N,S,NE,NW,SE,SW`,
+    `%.17g` (exact). `w` is the (9, ncy, ncx) plane stack of build_ismg_operator."""
+    import numpy as _np
+    w = _np.asarray(w).reshape(9, ncy, ncx)
+    out = ["ci,cj,C,E,W,N,S,NE,NW,SE,SW\n"]
+    for J in range(ncy):
+        for I in range(ncx):
+            out.append("%d,%d,%s\n" % (I, J, ",".join("%.17g" % float(w[sl, J, I]) for sl in range(9))))
+    s = "".join(out)
+    if isinstance(path_or_stream, str):
+        with _open(path_or_stream) as os_:
+            os_.write(s)
+    elif path_or_stream is not None:
+        path_or_stream.write(s)
+    return s
+
+
+# --------------------------------------------------------------------------
 # projection.hpp / bench.hpp
 
 

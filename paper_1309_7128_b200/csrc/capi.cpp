@@ -412,6 +412,21 @@ int ismg_bench_fine_pass(ismg_solver* s, ismg_field* x, const ismg_field* b, int
     });
 }
 
+int ismg_bench_coarse_visit(ismg_solver* s, const ismg_field* cb, ismg_field* ce, int64_t budget, int first_group,
+                            int64_t* sweeps, double* rc, double* ms) {
+    return guard([&] {
+        Solver& v = S(s);
+        need(sweeps, "sweeps");
+        need(rc, "rc");
+        need(ms, "ms");
+        if (!v.fused) fail(ISMG_ERR_INVALID_ARGUMENT, "bench_coarse_visit: solver has no fused path");
+        ISMG_CUDA(cudaSetDevice(v.ctx->device));
+        long long n = 0;
+        *ms = fused_bench_coarse_visit(v, F(cb), F(ce), budget, first_group, &n, rc);
+        *sweeps = n;
+    });
+}
+
 int ismg_ctx_launch_count(const ismg_ctx* c, int64_t* out) {
     return guard([&] {
         need(c, "ctx");

@@ -2,6 +2,8 @@
 // capture of [coarse-visit, fine-pass] slots, and the solve driver that polls
 // the device-resident phase once per graph launch.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -23,7 +25,9 @@ struct FusedEngine {
     int fine_launches = 1;  // kernels per fine slot (single-GPU one-warp pass: prolongation + sweep)
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
-    int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands
+    int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands,
+                             // 4 register wavefront over many SMs
+    RwEngine* rw = nullptr;
     TmGeom tm{};
     ClGeom cl{};
     // hybrid coarse visits: a one-SM kernel (cl1, role 1) runs groups of <= 4
@@ -85,16 +89,18 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     cudaGraph_t g;
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
-        if (e.coarse_kind == 3 && e.cl_hybrid)
-            launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
-        if (e.coarse_kind == 3)
+        if (e.coarse_kind == 4) {
+            launch_coarse_rw(e.P, *e.rw, c.stream);
+        } else if (e.coarse_kind == 3) {
+            if (e.cl_hybrid) launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
             launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-        else if (e.coarse_kind == 2)
+        } else if (e.coarse_kind == 2) {
             launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-        else if (e.coarse_kind == 1)
+        } else if (e.coarse_kind == 1) {
             launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
-        else
+        } else {
             launch_coarse_global(e.P, c.stream);
+        }
         e.fine_launches = launch_fine(e, c.stream);
         if (e.P.mp) mp_exchange(e, c);
     }
@@ -241,11 +247,14 @@ FusedEngine* make_fused(Solver& s) {
     // coarse-visit kernel: TMEM-resident rhs when the operator allows it,
     // else shared-memory iterate, else the global-memory wavefront
     std::vector<double> spec;
-    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "cl" | "tmem" | "smem" | "global"
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "rw" | "cl" | "tmem" | "smem" | "global"
+    const bool allow_rw = !force || std::string(force) == "rw";
     const bool allow_cl = !force || std::string(force) == "cl";
     const bool allow_tmem = !force || std::string(force) == "tmem";
     const bool allow_smem = !force || std::string(force) == "smem" || std::string(force) == "tmem";
-    if (allow_cl && cl_coarse_plan(L.h, e->cl, spec, e->coarse_smem)) {
+    if (allow_rw && (e->rw = rw_try_create(L.h, c.device)) != nullptr) {
+        e->coarse_kind = 4;
+    } else if (allow_cl && cl_coarse_plan(L.h, e->cl, spec, e->coarse_smem)) {
         e->coarse_kind = 3;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
         ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
@@ -293,6 +302,7 @@ void destroy_fused(FusedEngine* e) {
     cudaFree(e->coarse_backup);
     cudaFree(e->tm_spec);
     cudaFree(e->coarse_backup1);
+    rw_destroy(e->rw);
     for (void* p : e->peer_map)
         if (p) cudaIpcCloseMemHandle(p);
     cudaFree(e->xbuf);
@@ -343,6 +353,73 @@ double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters) {
         c.sync();
     }
     return total / iters;
+}
+
+// Measurement / parity hook: ONE coarse visit of this engine's coarse-visit
+// kernel on rhs cb from ce = 0, at most `budget` sweeps, first group `first`
+// sweeps; ce receives the iterate. Returns the kernel's CUDA-event time (ms).
+double fused_bench_coarse_visit(Solver& s, const Field& cb, Field& ce, long long budget, int first,
+                                long long* sweeps, double* rc) {
+    FusedEngine& e = *s.fused;
+    Ctx& c = *s.ctx;
+    LevelDev& L = s.levels.front();
+    if (cb.nx != L.h.ncx || cb.ny != L.h.ncy || ce.nx != L.h.ncx || ce.ny != L.h.ncy)
+        fail(ISMG_ERR_INVALID_ARGUMENT, "bench_coarse_visit: fields must have the coarse extent");
+    if (budget < 1 || first < 1) fail(ISMG_ERR_INVALID_ARGUMENT, "bench_coarse_visit: budget, first >= 1");
+    const size_t w = sizeof(double) * size_t(L.h.ncx);
+    ISMG_CUDA(cudaMemcpy2DAsync(L.b->buf.origin(), sizeof(double) * L.b->buf.pitch, cb.buf.origin(),
+                                sizeof(double) * cb.buf.pitch, w, size_t(L.h.ncy), cudaMemcpyDeviceToDevice,
+                                c.stream));
+    std::vector<double> h(size_t(L.h.ncx) * L.h.ncy);
+    ISMG_CUDA(cudaMemcpy2DAsync(h.data(), w, cb.buf.origin(), sizeof(double) * cb.buf.pitch, w, size_t(L.h.ncy),
+                                cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    double rc0 = 0.0;
+    for (double v : h) rc0 = (rc0 < std::abs(v)) ? std::abs(v) : rc0;  // coarse_residual(ce = 0)
+    Ctl init{};
+    init.phase = kCoarse;
+    init.rc = rc0;
+    init.pred = first;
+    init.total = e.P.max_total - budget;
+    init.nvisits = 1;
+    *e.h_ctl = init;
+    ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    cudaEvent_t e0, e1;
+    ISMG_CUDA(cudaEventCreate(&e0));
+    ISMG_CUDA(cudaEventCreate(&e1));
+    ISMG_CUDA(cudaEventRecord(e0, c.stream));
+    if (e.coarse_kind == 4) {
+        launch_coarse_rw(e.P, *e.rw, c.stream);
+    } else if (e.coarse_kind == 3) {
+        if (e.cl_hybrid) launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
+        launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
+    } else if (e.coarse_kind == 2) {
+        launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
+    } else if (e.coarse_kind == 1) {
+        launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
+    } else {
+        launch_coarse_global(e.P, c.stream);
+    }
+    ISMG_CUDA(cudaEventRecord(e1, c.stream));
+    ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    ISMG_CUDA(cudaMemcpy2DAsync(ce.buf.origin(), sizeof(double) * ce.buf.pitch, L.x->buf.origin(),
+                                sizeof(double) * L.x->buf.pitch, w, size_t(L.h.ncy), cudaMemcpyDeviceToDevice,
+                                c.stream));
+    c.sync();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (e.h_ctl->mp_error == 2) fail(ISMG_ERR_INTERNAL, "coarse visit: watchdog (mailbox / barrier timeout)");
+    if (e.coarse_kind == 4 && getenv("ISMG_RW_TRACE")) {  // debug: per-group residual maxima to stderr
+        const std::vector<double> t = rw_trace_take();
+        for (double v : t) fprintf(stderr, v == -1.0 ? "\nRWTRACE" : (v == -2.0 ? "\nRWSLOW" : " %.17g"), v);
+        fprintf(stderr, "\n");
+    }
+    *sweeps = e.h_ctl->coarse;
+    *rc = e.h_ctl->rc;
+    s.last.coarse_engine = e.coarse_kind;
+    return ms;
 }
 
 void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics& M, bool, double**) {
@@ -406,6 +483,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     ISMG_CUDA(cudaGetLastError());
     const Ctl& st = *e.h_ctl;
     e.mp_seq = st.mp_seq;
+    if (st.mp_error == 2) fail(ISMG_ERR_INTERNAL, "coarse visit: a mailbox word or grid barrier timed out (watchdog)");
     if (st.mp_error) fail(ISMG_ERR_INTERNAL, "multi-GPU: a peer's pack did not arrive (exchange timed out)");
     // replay the sweep sequence into the metrics (lap_equiv order, metrics.hpp:46-56)
     const int nv = std::min(st.nvisits, e.P.visit_cap);
@@ -433,6 +511,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.coarse_visits = st.coarse_launches;
     s.last.coarse_ms = double(st.coarse_ns) * 1e-6;
     s.last.coarse_steps = st.coarse_steps;
+    s.last.coarse_engine = e.coarse_kind;
     s.last.collectives = c.comm ? c.comm->collectives : 0;
     s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
     s.last.kernel_launches = ((e.P.mp ? 3 : 2) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;

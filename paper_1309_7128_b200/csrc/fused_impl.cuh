@@ -338,6 +338,14 @@ void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, doub
                       cudaStream_t st);
 void set_coarse_cl_smem(size_t bytes);
 
+// Register-wavefront coarse visit over many SMs (coarse_rw.cu); nullptr when
+// the operator does not fit it (then a cluster / TMEM / smem / global engine).
+struct RwEngine;
+RwEngine* rw_try_create(const CoarseOpH& op, int device);
+void rw_destroy(RwEngine* e);
+void launch_coarse_rw(const Params& P, const RwEngine& e, cudaStream_t st);
+std::vector<double> rw_trace_take();
+
 bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem);
 void launch_coarse_tmem(const Params& P, const TmGeom& T, const double* spec, double* backup, size_t smem,
                         cudaStream_t st);

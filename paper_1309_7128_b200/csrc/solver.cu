@@ -73,7 +73,7 @@ Solver::Solver(Ctx* c, const ismg_grid_spec& g0, const ismg_cycle_config& cfg0) 
 
 Solver::~Solver() {
     cudaSetDevice(ctx->device);
-    ctx->sync();
+    cudaStreamSynchronize(ctx->stream);  // no throw from a destructor (the context may be torn down at exit)
     destroy_fused(fused);
     fused = nullptr;
     for (auto& L : levels) L.release();
@@ -140,6 +140,7 @@ void Solver::solve(Field& x, const Field& b, ismg_report& rep, ismg_step_metrics
     ISMG_CUDA(cudaSetDevice(ctx->device));
     rep = ismg_report{1, 0, 0, 0, 0.0};
     last = ismg_solve_stats{};
+    last.coarse_engine = -1;
     Metrics M{m, fine_cells > 0 ? fine_cells : int64_t(g.nx) * g.ny};
     cudaEvent_t e0, e1;
     ISMG_CUDA(cudaEventCreate(&e0));

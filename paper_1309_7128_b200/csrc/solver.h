@@ -95,5 +95,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
                  double** pending_shift);
 void destroy_fused(FusedEngine* e);
 double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters);
+double fused_bench_coarse_visit(Solver& s, const Field& cb, Field& ce, long long budget, int first,
+                                long long* sweeps, double* rc);
 
 }  // namespace ismgb

@@ -199,6 +199,14 @@ class PressureSolver:
         _lib.call("ismg_bench_fine_pass", self.h, x.h, b.h, int(iters), C.byref(ms))
         return ms.value
 
+    def bench_coarse_visit(self, cb: DeviceField, ce: DeviceField, budget: int, first_group: int = 1):
+        """One coarse visit of the fused engine on rhs cb from ce = 0 (coarse extent);
+        returns (sweeps, final coarse residual max, kernel ms)."""
+        n, rc, ms = C.c_int64(), C.c_double(), C.c_double()
+        _lib.call("ismg_bench_coarse_visit", self.h, cb.h, ce.h, int(budget), int(first_group), C.byref(n),
+                  C.byref(rc), C.byref(ms))
+        return n.value, rc.value, ms.value
+
     def visit_log(self):
         """[(coarse sweeps, fine sweeps)] per outer iteration of the last fused solve."""
         n = C.c_size_t()

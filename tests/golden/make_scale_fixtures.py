@@ -54,7 +54,7 @@ def cases():
     return {
         "c1": (lid(256, 100.0), 16, 1500, 0, 1500),       # BASELINE config 1, every step of the run
         "c2": (lid(4096, 1000.0), 32, 3, 16, 1),          # config 2, steps 1-3
-        "c3": (lid(16384, 1000.0), 32, 2, 64, 1),         # config 3, steps 1-2
+        "c3": (lid(16384, 1000.0), 32, 3, 64, 1),         # config 3, steps 1-3
         "jet512": (jet(512, 1024), 16, 12, 4, 1),         # config 4 scaled (coarse 32x64)
         "jet1024": (jet(1024, 2048), 16, 20, 8, 1),       # config 4 scaled (coarse 64x128)
         "c4": (jet(8192, 16384), 16, 1, 64, 1),           # config 4 full size, step 1

@@ -12,8 +12,9 @@ downloads the state after every step and compares:
   * the closed metrics row (step, I_f, I_c, NCC_f, NCC_c, restrictions,
     prolongations, converged) — identical;
   * N_Lap (1e-12) and residual_final (a cancellation-amplified diagnostic, 1e-6);
-  * u, v, p: full-array L2 norm, the full middle row and column, and (after
-    step 1 and the last step) a strided sample — each within 1e-10 relative L2.
+  * u, v, p: full-array L2 norm, the full middle row and column (error over the
+    whole field's norm), and (after step 1 and the last step) a strided sample —
+    each within 1e-10 relative L2.
     Config 1 (256^2) compares the full fields.
 """
 import os
@@ -81,8 +82,11 @@ def run_and_compare(P, name):
             key = "step%d/%s/" % (k, fname)
             n_ref = float(z[key + "norm"][0])
             errs.append((k, fname, "norm", abs(np.linalg.norm(arr) - n_ref) / max(n_ref, 1e-300)))
-            errs.append((k, fname, "row", rel_l2(arr[arr.shape[0] // 2], z[key + "row"])))
-            errs.append((k, fname, "col", rel_l2(arr[:, arr.shape[1] // 2], z[key + "col"])))
+            # the middle row / column against the WHOLE field's norm (the north star's
+            # relative L2 is of the field; a column on a symmetry line is ~0 on its own)
+            for what, got, ref in (("row", arr[arr.shape[0] // 2], z[key + "row"]),
+                                   ("col", arr[:, arr.shape[1] // 2], z[key + "col"])):
+                errs.append((k, fname, what, float(np.linalg.norm(got - ref)) / max(n_ref, 1e-300)))
             if key + "samp" in z:
                 o = stride // 2
                 errs.append((k, fname, "samp", rel_l2(arr[o::stride, o::stride], z[key + "samp"])))
@@ -100,8 +104,8 @@ def run_and_compare(P, name):
     # in it amplified; it is a diagnostic, checked to 1e-6 relative
     assert rel_l2(got_f[:, 1], z["rowsf"][:, 1]) <= 1e-6
     if stride:
-        worst = max(errs, key=lambda e: e[3])
-        assert worst[3] <= REL_L2, "worst field error %s" % (worst,)
+        over = sorted([e for e in errs if not e[3] <= REL_L2], key=lambda e: -e[3])
+        assert not over, "field errors above %g (step, field, what, rel): %s" % (REL_L2, over[:8])
     else:
         st = res.state
         for a, key in ((st.vel.u_data, "u"), (st.vel.v_data, "v"), (st.p.data, "p")):
@@ -131,8 +135,8 @@ def test_jet1024x2048_20_steps(dev):
 
 
 @pytest.mark.slow
-def test_config3_lid16384_steps_1_2(dev):
-    """BASELINE config 3 (16384^2, coarse 512^2), steps 1-2."""
+def test_config3_lid16384_steps_1_to_3(dev):
+    """BASELINE config 3 (16384^2, coarse 512^2), steps 1-3."""
     run_and_compare(dev, "c3")
 
 

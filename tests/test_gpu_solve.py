@@ -193,3 +193,40 @@ def test_coarse_cluster_plans_match_oracle(dev, port, monkeypatch, n, tile, env)
     for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
                  (res.state.p.data, st.p.data)):
         assert rel_l2(a, b) <= REL_L2
+
+
+@pytest.mark.parametrize("case_name,nsteps", [("lid256t4", 3), ("lid512t4", 2), ("jet256x512t4", 4),
+                                              ("lid1024t4", 1)])
+def test_coarse_register_wavefront_matches_oracle(dev, port, monkeypatch, case_name, nsteps):
+    """The register-wavefront coarse engine (coarse_rw.cu) on coarse grids of
+    64^2 (2 lane segments per row, 32 warps), 128^2, a rectangular non-singular
+    jet 64x128 with Dirichlet closures on the top rows, and 256^2 (8 segments,
+    128 warps over 32 CTAs): per-step counts equal the reference's and fields
+    match within the north star's tolerance."""
+    P = dev
+    monkeypatch.setenv("ISMG_COARSE_KERNEL", "rw")
+    if case_name.startswith("lid"):
+        n = int(case_name[3:].split("t")[0])
+        case = setup_lid_cavity(n, 1000.0)
+        case.dt = 1000.0 / n
+    else:
+        case = setup_jet(256, 512, 0.1, 8)
+    cfg = CycleConfig(tile=4)
+    case.steps, case.t_max, case.steady_tol = nsteps, 0.0, 0.0
+    res = P.run_case(case, cfg)
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, _ = port.run_steps(case.grid, cfg, st, nsteps)
+    got = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in res.metrics.rows]
+    want = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in rows]
+    assert got == want
+    for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
+                 (res.state.p.data, st.p.data)):
+        assert rel_l2(a, b) <= REL_L2
+    # the solve ran on the register-wavefront engine
+    solver = P.PressureSolver(case.grid, cfg)
+    x = ScalarField(case.grid.nx, case.grid.ny)
+    b = random_field(case.grid.nx, case.grid.ny, np.random.default_rng(5))
+    b.shift_interior(-b.interior_mean())
+    solver.solve(x, b, RunMetrics(case.grid.nx * case.grid.ny))
+    assert solver.last_stats()["coarse_engine"] == 4

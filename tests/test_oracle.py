@@ -7,6 +7,8 @@
    generator tests/golden/make_golden.py) — bit-exact.
 3. Port == reference bit-for-bit on fresh random cases, when oracle/_ref is built.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -446,14 +448,81 @@ def test_bench_fine_iteration_sample(port, ref):
     assert np.array_equal(x_ref.data, x_port.data)
 
 
-def test_bench_jet_workload_and_sample(port, ref):
-    """bench.py --case jet (config 4): setup_jet(n, 2n, 0.1, 16) (bench.hpp:73-88), tile 16
-    (jet.cfg:15); the bounded fine-iteration sample runs on the nx x 2nx grid and the
-    reference and the port land on the same fine sweep count."""
+def test_bench_workloads():
+    """bench.py: the default line is BASELINE config 3 (lid 16384^2, tile 32); --case jet is
+    config 4 (setup_jet(8192, 16384, 0.1, 16), bench.hpp:73-88, tile 16, jet.cfg:15); an explicit
+    --grid always wins (jet --grid 4096 is 4096 x 8192)."""
+    import argparse
     import bench
+    ns = lambda **k: argparse.Namespace(**{"case": "lid", "grid": None, **k})  # noqa: E731
+    assert bench.grid_side(ns()) == 16384
+    assert bench.grid_side(ns(case="jet")) == 8192
+    assert bench.grid_side(ns(case="jet", grid=4096)) == 4096
+    assert bench.grid_side(ns(grid=4096)) == 4096
     case, cfg = bench.workload(bench.JET_NX, "jet")
     assert (case.grid.nx, case.grid.ny, cfg.tile) == (8192, 16384, 16)
     assert "config 4" in bench.workload_desc(bench.JET_NX, "jet")
-    for kind in ("reference", "port"):
-        i_f, secs = bench.cpu_fine_iterations(kind, 32, 2, "jet")
-        assert i_f == 2 and secs >= 0.0
+    case, cfg = bench.workload(16384, "lid")
+    assert (case.grid.nx, cfg.tile, case.dt) == (16384, 32, 1000.0 / 16384)
+    assert "config 3" in bench.workload_desc(16384, "lid")
+
+
+def test_bench_cpu_model_tracks_the_reference(ref):
+    """bench.py's same-work CPU baseline: the reference's per-operation costs (ref_op_costs)
+    times a run's per-step counts reproduce the reference's own wall time of that run."""
+    import bench
+    from paper_1309_7128_b200.api import FluidState
+    n = 256
+    case, cfg = bench.workload(n, "lid")
+    o = ref.op_costs(case.grid, cfg, case.dt, case.nu, 3)
+    assert o.shape == (9,) and (o > 0).all()
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, secs = ref.run_steps(case.grid, cfg, st, 4)
+    counts = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations) for r in rows]
+    t = bench.model_seconds(o, counts)
+    assert 0.4 * secs <= t <= 1.6 * secs, (t, secs)
+
+
+def test_bench_reference_counts_are_the_references():
+    """The reference arm's per-step counts come from the reference's own fixtures first."""
+    import bench
+    import numpy as np
+    rows, src = bench.reference_counts(4096, "lid", 3)
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "scale", "c2.npz"))
+    assert rows == [(int(r[1]), int(r[2]), int(r[5]), int(r[6])) for r in z["rows"]]
+    assert "c2.npz" in src
+    rows5, src5 = bench.reference_counts(4096, "lid", 5)
+    assert rows5[:3] == rows and len(rows5) == 5
+
+
+@pytest.mark.parametrize("which", ["lid", "jet"])
+def test_writers_match_the_reference_bytes(ref, tmp_path, which):
+    """io.hpp:35-117: write_field_csv, write_vtk and write_operator_csv (`%.17g`, the
+    exact-coefficient dump) produce the reference's bytes on a stepped state."""
+    import ctypes as C
+    from paper_1309_7128_b200 import api
+    from paper_1309_7128_b200._abi import dptr
+    if which == "lid":
+        case = api.setup_lid_cavity(24, 100.0)
+        case.dt = 100.0 / 24
+        tile = 4
+    else:
+        case = api.setup_jet(20, 40, 0.1, 4)
+        tile = 4
+    g = case.grid.copy()
+    g.tile = tile
+    st = api.FluidState(g)
+    st.dt, st.nu = case.dt, case.nu
+    ref.run_steps(g, api.CycleConfig(tile=tile), st, 3)
+    paths = [str(tmp_path / ("ref_" + n)) for n in ("p.csv", "s.vtk", "op.csv")]
+    rc = ref._fn("write_outputs")(C.byref(g.to_c()), dptr(st.vel.u_data), dptr(st.vel.v_data), dptr(st.p.data),
+                                  *[q.encode() for q in paths])
+    assert rc == 0
+    mine = [str(tmp_path / ("our_" + n)) for n in ("p.csv", "s.vtk", "op.csv")]
+    api.write_field_csv(st.p, g, mine[0])
+    api.write_vtk(st.p, st.vel, g, mine[1])
+    ncx, ncy, w = ref.build_ismg_operator(g)
+    api.write_operator_csv(ncx, ncy, w, mine[2])
+    for a, b in zip(paths, mine):
+        assert open(a, "rb").read() == open(b, "rb").read(), b
