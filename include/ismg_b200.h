@@ -20,9 +20,9 @@
  *   - fields live on the device with the reference's logical layout (one
  *     ghost ring around an nx x ny interior); host arrays passed to
  *     upload/download use exactly the reference layout:
- *       scalar  (nx+2)*(ny+2), index (j+1)*(nx+2) + (i+1)     field.hpp:175-182
- *       u       (nx+3)*(ny+2), index (j+1)*(nx+3) + (i+1)     field.hpp:262-266
- *       v       (nx+2)*(ny+3), index (j+1)*(nx+2) + (i+1)     field.hpp:263-268
+ *       scalar  (nx+2)*(ny+2), index (j+1)*(nx+2) + (i+1)     field.hpp:24-31
+ *       u       (nx+3)*(ny+2), index (j+1)*(nx+3) + (i+1)     field.hpp:108-117
+ *       v       (nx+2)*(ny+3), index (j+1)*(nx+2) + (i+1)     field.hpp:108-117
  *   - one context per host thread; there is no global mutable state apart
  *     from the thread-local error string.
  *

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_visit_kernel(Params P) 
             s->prev = s->r;
             s->phase = kFine;
         }
+        publish_phase(P, s->phase);
     }
 }
 
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(kCoarseSmemThreads) coarse_visit_smem_kernel(P
             s->prev = s->r;
             s->phase = kFine;
         }
+        publish_phase(P, s->phase);
     }
 }
 

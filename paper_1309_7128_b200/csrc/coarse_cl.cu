@@ -176,9 +176,7 @@ __device__ __forceinline__ double apply_lane(const Wts& W, const Nbr& v, double 
     const double num = bIJ - acc;
     if (kResidual) return num;
     if (!fastdiv) return num / W.w[0];
-    const double q = __dmul_rn(num, W.y);  // Markstein: exact RN(num / w0) (host-verified per divisor)
-    const double r = __fma_rn(-q, W.w[0], num);
-    return __fma_rn(r, W.y, q);
+    return div_cr(num, W.w[0], W.y);  // correctly rounded (kernels.cuh)
 }
 
 // One group of G sweeps (residuals: also form the residual max of every sweep).
@@ -668,6 +666,7 @@ __global__ void __launch_bounds__(kClThreads, 1) coarse_cl_kernel(Params P, ClGe
             st->prev = st->r;
             st->phase = kFine;
         }
+        publish_phase(P, st->phase);
     }
 }
 
@@ -729,7 +728,7 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     for (int J = 0; J < op.ncy; ++J) classify(2 * op.ncx + J, 0, J), classify(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
     T.ncls = int(cls.size());
     if (T.ncls > 1024) return false;
-    T.fastdiv = 1;  // Markstein's correction per divisor (ring classes and the interior), spot-checked
+    T.fastdiv = 1;  // div_cr (kernels.cuh): correctly rounded for every divisor; the sample below is a sanity check
     T.stdy = 1.0 / T.stdw[0];
     uint64_t st = 0x9E3779B97F4A7C15ull;
     for (size_t c = 0; c <= cls.size(); ++c) {

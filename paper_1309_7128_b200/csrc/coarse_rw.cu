@@ -60,9 +60,9 @@ namespace {
 
 constexpr int kLS = 32;    // columns per lane segment = sweep lag
 constexpr int kR = 2;      // rows per warp
-constexpr int kRl = 24;    // residual lag (steps)
+constexpr int kRl = 28;    // residual lag (steps): the largest the in-warp overwrite allows (kLS - 4)
 constexpr int kA = 4;      // mailbox prefetch distance (steps)
-constexpr int kM = 4;      // extra lead restored after a stall on the row below (steps)
+constexpr int kM = 1;      // extra lead restored after a stall on the row below (steps)
 constexpr int kNS = 8;     // prefetch slots per stream (power of two, > kA)
 constexpr int kNStr = 4;   // mailbox streams: update-south, residual-south, update-north, residual-north
 constexpr int kMaxG = 4096;
@@ -241,7 +241,7 @@ __device__ __forceinline__ bool ll_wait(const char* word, unsigned tag, long lon
 
 __device__ double g_rw_trace[8192];
 __device__ unsigned g_rw_trace_n;
-__device__ unsigned long long g_rw_slow[2];  // slow-path entries: [0] stale words, [1] waits ahead (debug counters)
+__device__ unsigned long long g_rw_slow[6];  // debug counters: slow-path entries by stream [0..3], own-column words [4], waits ahead [5]
 
 // Slow path (warp-uniform): re-read a stale mailbox word until the writer's tag
 // shows and put it back into its slot (read again by later steps / the lane
@@ -250,9 +250,13 @@ __device__ unsigned long long g_rw_slow[2];  // slow-path entries: [0] stale wor
 // wait until the word kA + kM steps ahead has arrived, which restores kM steps
 // of slack for the copies issued from here on.
 __device__ __noinline__ void ll_settle(uint32_t slot, const char* word, unsigned tag, bool bad, const char* ahead,
-                                       unsigned tag_ahead, bool wait_ahead) {
+                                       unsigned tag_ahead, bool wait_ahead, int stream) {
     const long long t0 = gtimer();
-    if (threadIdx.x % 32 == 0) atomicAdd(&g_rw_slow[wait_ahead ? 1 : 0], 1ull);
+    const bool any_wa = __any_sync(kFull, wait_ahead);
+    if (threadIdx.x % 32 == 0) {
+        atomicAdd(&g_rw_slow[stream], 1ull);
+        if (any_wa) atomicAdd(&g_rw_slow[5], 1ull);
+    }
     if (bad) {
         uint4 u;
         for (;;) {
@@ -285,13 +289,13 @@ __device__ __forceinline__ void pf_check(const Lane& L, const Per& p, bool resid
         const char* ahead = mb_word<S>(L, p, ca + 1, da);
         const uint4 u = lds_u4(sl);
         const bool bad = want && ((u.y ^ tag) | (u.w ^ tag)) != 0u;
-        if (__any_sync(kFull, bad)) ll_settle(sl, mb_word<S>(L, p, c + 1, d), tag, bad, ahead, p.tq + unsigned(da), wa);
+        if (__any_sync(kFull, bad)) ll_settle(sl, mb_word<S>(L, p, c + 1, d), tag, bad, ahead, p.tq + unsigned(da), wa, S);
         if constexpr (c == 0) {
             const bool own = act && L.lane == 0;
             const uint4 v = lds_u4(sl + 16u * 32u);
             const bool bad0 = own && ((v.y ^ tag) | (v.w ^ tag)) != 0u;
             if (__any_sync(kFull, bad0))
-                ll_settle(sl + 16u * 32u, mb_word<S>(L, p, 0, d), tag, bad0, ahead, p.tq + unsigned(da), wa);
+                ll_settle(sl + 16u * 32u, mb_word<S>(L, p, 0, d), tag, bad0, ahead, p.tq + unsigned(da), wa, 4);
         }
     }
 }
@@ -324,24 +328,6 @@ __device__ __forceinline__ double wval(const Lane& L) {
             return v;
         }
     }
-}
-
-// Correctly rounded num / w (see the header), y = RN(1 / w): the exponent of
-// num decides (integer test); a warp-uniform branch takes IEEE division for
-// any lane outside [2^-900, 2^1000].
-__device__ __noinline__ double div_ieee(double num, double w, double q, bool bad) {
-    return bad ? __ddiv_rn(num, w) : q;
-}
-__device__ __forceinline__ double div_cr(double num, double w, double y) {
-    const unsigned e = unsigned(__double2hiint(num)) & 0x7ff00000u;
-    const bool bad = e - (123u << 20) > (1900u << 20);
-    const double q0 = __dmul_rn(num, y);
-    const double e0 = __fma_rn(-q0, w, num);
-    const double q1 = __fma_rn(e0, y, q0);
-    const double e1 = __fma_rn(-q1, w, num);
-    double q = __fma_rn(e1, y, q1);
-    if (__any_sync(kFull, bad)) q = div_ieee(num, w, q, bad);
-    return q;
 }
 
 // Interior weights (slot order C, E, W, N, S, NE, NW, SE, SW): the ISMG
@@ -773,6 +759,7 @@ __global__ void __launch_bounds__(kRwThreads, 1) coarse_rw_kernel(Params P, RwK 
             st->prev = st->r;
             st->phase = kFine;
         }
+        publish_phase(P, st->phase);
     }
 }
 
@@ -885,10 +872,11 @@ std::vector<double> rw_trace_take() {
     if (n) ISMG_CUDA(cudaMemcpyFromSymbol(v.data(), g_rw_trace, sizeof(double) * n));
     const unsigned z = 0;
     ISMG_CUDA(cudaMemcpyToSymbol(g_rw_trace_n, &z, sizeof(unsigned)));
-    unsigned long long slow[2] = {0, 0};
+    unsigned long long slow[6] = {0, 0, 0, 0, 0, 0};
     ISMG_CUDA(cudaMemcpyFromSymbol(slow, g_rw_slow, sizeof(slow)));
-    v.push_back(-2.0), v.push_back(double(slow[0])), v.push_back(double(slow[1]));
-    const unsigned long long z2[2] = {0, 0};
+    v.push_back(-2.0);
+    for (unsigned long long c : slow) v.push_back(double(c));
+    const unsigned long long z2[6] = {0, 0, 0, 0, 0, 0};
     ISMG_CUDA(cudaMemcpyToSymbol(g_rw_slow, z2, sizeof(z2)));
     return v;
 }

@@ -110,14 +110,10 @@ __device__ __forceinline__ double apply_w(const double* w, const Nbr& v, double 
 }
 
 // a / -3 correctly rounded, without the DDIV sequence (~115-cycle latency):
-// Markstein's correction with y = RN(1/b): q = RN(a y), r = a - b q (exact by
-// FMA), RN(q + r y) = RN(a / b). Checked against __ddiv_rn bit for bit on
-// 1.2e9 random operands per divisor (tools/verify_div3.cu).
+// div_cr (kernels.cuh), two Markstein corrections with y = RN(-1/3).
 __device__ __forceinline__ double div_m3(double a) {
     constexpr double y = -1.0 / 3.0;
-    const double q = __dmul_rn(a, y);
-    const double r = __fma_rn(-q, -3.0, a);
-    return __fma_rn(r, y, q);
+    return div_cr(a, -3.0, y);
 }
 
 // Compile-time interior stencils (host-verified against the built operator).
@@ -172,10 +168,7 @@ __device__ __forceinline__ double tm_cell(const TmGeom& T, const double* rc, con
     }
     const double num = bIJ - acc;
     if (!T.fastdiv) return num / w[0];
-    const double y = wc[9];  // Markstein: exact RN(num / w0)
-    const double q = __dmul_rn(num, y);
-    const double r = __fma_rn(-q, w[0], num);
-    return __fma_rn(r, y, q);
+    return div_cr(num, w[0], wc[9]);  // correctly rounded (kernels.cuh)
 }
 
 // max over the warp of non-negative doubles through two 32-bit REDUX steps
@@ -454,6 +447,7 @@ __global__ void __launch_bounds__(kTmThreads) coarse_visit_tmem_kernel(Params P,
             st->prev = st->r;
             st->phase = kFine;
         }
+        publish_phase(P, st->phase);
     }
 }
 

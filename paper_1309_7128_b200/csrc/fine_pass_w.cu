@@ -722,13 +722,14 @@ dim3 fine_pass_w_grid(const Params& P) {
     const int W = 4 * fine_pass_w_quads(P.tile);
     return dim3((P.nx + W - 1) / W, P.nchunks);
 }
-int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only) {
+int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only, bool ph2_only) {
     const int nq = fine_pass_w_quads(P.tile);
     if (P.mp) {
         fine_pass_w_kernel<true, 0><<<grid, 32, 0, st>>>(P, nq);
         return 1;
     }
     if (!sweep_only) fine_pass_w_kernel<false, 2><<<grid, 32, 0, st>>>(P, nq);
+    if (ph2_only) return 1;
     fine_pass_w_kernel<false, 0><<<grid, 32, 0, st>>>(P, nq);
     return sweep_only ? 1 : 2;
 }

@@ -22,6 +22,10 @@ struct FusedEngine {
     int* d_log = nullptr;
     std::vector<int> h_log;
     cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // 8, 16, 32, 64 slots, captured once
+    // single GPU: one conditional graph per solve, WHILE(phase != done) { SWITCH(phase) }
+    // (state 0 not built yet, 1 built, -1 unavailable: the slot graphs above)
+    cudaGraphExec_t cond_exec = nullptr;
+    int cond_state = 0;
     int fine_launches = 1;  // kernels per fine slot (single-GPU one-warp pass: prolongation + sweep)
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
@@ -69,6 +73,73 @@ static int launch_fine(const FusedEngine& e, cudaStream_t st, bool sweep_only = 
     return 1;
 }
 
+// the coarse-visit kernel(s) of this engine with parameters P
+static void launch_coarse(const FusedEngine& e, const Params& P, cudaStream_t st) {
+    if (e.coarse_kind == 4) {
+        launch_coarse_rw(P, *e.rw, st);
+    } else if (e.coarse_kind == 3) {
+        if (e.cl_hybrid) launch_coarse_cl(P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, st);
+        launch_coarse_cl(P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, st);
+    } else if (e.coarse_kind == 2) {
+        launch_coarse_tmem(P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, st);
+    } else if (e.coarse_kind == 1) {
+        launch_coarse_smem(P, e.coarse_backup, e.coarse_smem, st);
+    } else {
+        launch_coarse_global(P, st);
+    }
+}
+
+// The single-GPU solve as ONE conditional graph: WHILE (phase != done) {
+// SWITCH (phase) { kFine: sweep pass | kCoarse: coarse visit | kProlong,
+// kResid: prolongation / residual pass } }. The kernel that decides the next
+// phase sets both conditions (publish_phase), so every launch does work and
+// the host waits once per solve. Returns false where conditional nodes are
+// unavailable (the slot graphs then run the solve).
+static bool build_cond_graph(FusedEngine& e) {
+    Ctx& c = *e.s->ctx;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+    cudaGraphConditionalHandle hw = 0, hs = 0;
+    ok = ok && cudaGraphConditionalHandleCreate(&hw, g, 1u, cudaGraphCondAssignDefault) == cudaSuccess;
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wn = nullptr, sn = nullptr;
+    ok = ok && cudaGraphAddNode(&wn, g, nullptr, 0, &wp) == cudaSuccess;
+    cudaGraph_t body = ok ? wp.conditional.phGraph_out[0] : nullptr;
+    ok = ok && cudaGraphConditionalHandleCreate(&hs, body, unsigned(kResid), cudaGraphCondAssignDefault) == cudaSuccess;
+    cudaGraphNodeParams sp = {};
+    sp.type = cudaGraphNodeTypeConditional;
+    sp.conditional.handle = hs;
+    sp.conditional.type = cudaGraphCondTypeSwitch;
+    sp.conditional.size = 4;  // kFine, kCoarse, kProlong, kResid; kDone runs no body
+    ok = ok && cudaGraphAddNode(&sn, body, nullptr, 0, &sp) == cudaSuccess;
+    if (ok) {
+        Params Pc = e.P;
+        Pc.cond = 1, Pc.h_while = hw, Pc.h_switch = hs;
+        for (int ph = 0; ph < 4 && ok; ++ph) {
+            ok = cudaStreamBeginCaptureToGraph(c.stream, sp.conditional.phGraph_out[ph], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (!ok) break;
+            if (ph == kCoarse) {
+                launch_coarse(e, Pc, c.stream);
+            } else if (e.fine_kind == 2) {
+                launch_fine_pass_w(Pc, e.grid, c.stream, ph == kFine, ph != kFine);
+            } else {
+                launch_fine_pass(Pc, e.grid, e.smem, c.stream);
+            }
+            cudaGraph_t tmp = nullptr;
+            ok = cudaStreamEndCapture(c.stream, &tmp) == cudaSuccess;
+        }
+    }
+    ok = ok && cudaGraphInstantiate(&e.cond_exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();  // a refused node type leaves no sticky error
+    return ok;
+}
+
 // multi-GPU, after every fine-pass slot: the fine pass has stored its pack into
 // every rank's exchange buffer (NVLink peer stores) and raised its flags;
 // mp_unpack_kernel waits for all ranks' flags, reduces the pass partials in rank
@@ -89,18 +160,7 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     cudaGraph_t g;
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
-        if (e.coarse_kind == 4) {
-            launch_coarse_rw(e.P, *e.rw, c.stream);
-        } else if (e.coarse_kind == 3) {
-            if (e.cl_hybrid) launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
-            launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-        } else if (e.coarse_kind == 2) {
-            launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-        } else if (e.coarse_kind == 1) {
-            launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
-        } else {
-            launch_coarse_global(e.P, c.stream);
-        }
+        launch_coarse(e, e.P, c.stream);
         e.fine_launches = launch_fine(e, c.stream);
         if (e.P.mp) mp_exchange(e, c);
     }
@@ -108,6 +168,107 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     ISMG_CUDA(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
     return ge;
+}
+
+// The coarse-visit kernel of level h: the cluster engine where it plans (coarse
+// grids up to 16 x 32-row bands), the register wavefront beyond it (config 4's
+// 512 x 1024 level), then TMEM-resident rhs, shared-memory iterate, global
+// wavefront. P.ncx / P.ncy must be set.
+static void plan_coarse(FusedEngine& ee, const CoarseOpH& h, int device) {
+    FusedEngine* e = &ee;
+    Params& P = e->P;
+    std::vector<double> spec;
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "rw" | "cl" | "tmem" | "smem" | "global"
+    const bool allow_rw = !force || std::string(force) == "rw";
+    const bool allow_cl = !force || std::string(force) == "cl";
+    const bool allow_tmem = !force || std::string(force) == "tmem";
+    const bool allow_smem = !force || std::string(force) == "smem" || std::string(force) == "tmem";
+    const bool force_rw = force && std::string(force) == "rw";
+    if (!force_rw && allow_cl && cl_coarse_plan(h, e->cl, spec, e->coarse_smem)) {
+        e->coarse_kind = 3;
+        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
+        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * cl_backup_doubles(e->cl)));
+        size_t smax = e->coarse_smem;
+        // hybrid when the grid also fits one SM and the cluster is 2 SMs: a 2048^2
+        // step 1 takes 170 ms with it against 181 without; at 4096^2 (4 SMs) the
+        // one-SM kernel's shorter small groups are eaten by the extra launch per
+        // slot (494 against 487 ms). ISMG_CL_HYBRID=0 / 1 forces it off / on.
+        const char* hy = getenv("ISMG_CL_HYBRID");
+        const bool want = hy ? std::string(hy) != "0" : e->cl.csize == 2;
+        std::vector<double> spec1;
+        if (e->cl.csize > 1 && want &&
+            cl_coarse_plan(h, e->cl1, spec1, e->coarse_smem1, 128) && e->cl1.csize == 1 && spec1 == spec) {
+            e->cl_hybrid = true;
+            e->cl1.role = 1, e->cl.role = 2;
+            ISMG_CUDA(cudaMalloc(&e->coarse_backup1, sizeof(double) * cl_backup_doubles(e->cl1)));
+            smax = std::max(smax, e->coarse_smem1);
+        }
+        set_coarse_cl_smem(smax);
+    } else if (allow_rw && (e->rw = rw_try_create(h, device)) != nullptr) {
+        e->coarse_kind = 4;
+    } else if (allow_tmem && tmem_coarse_plan(h, e->tm, spec, e->coarse_smem)) {
+        e->coarse_kind = 2;
+        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
+        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.pitch));
+        set_coarse_tmem_smem(e->coarse_smem);
+    } else if (allow_smem && size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double) <= 200 * 1024) {
+        e->coarse_kind = 1;
+        e->coarse_smem = size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double);
+        ISMG_CUDA(cudaMalloc(&e->coarse_backup, e->coarse_smem));
+        set_coarse_smem(e->coarse_smem);
+    }
+}
+
+// A coarse-visit engine alone, for level L of a solver (the ACM hierarchy's
+// coarsest level, cycles.hpp:222-235): the same kernels as the fused path's
+// coarse phase, on L's rhs / iterate, one launch and one wait per visit.
+FusedEngine* make_coarse_engine(Solver& s, LevelDev& L) {
+    auto* e = new FusedEngine();
+    e->s = &s;
+    Params& P = e->P;
+    P.ncx = L.h.ncx, P.ncy = L.h.ncy, P.tile = 1;
+    P.singular = L.h.singular ? 1 : 0;
+    P.nslots = L.h.stencil_points();
+    P.tol_fine = s.cfg.tol_fine, P.tol_coarse = s.cfg.tol_coarse, P.stall = s.cfg.stall_factor;
+    P.max_total = s.cfg.max_total_sweeps;
+    P.cb = L.b->view();
+    P.ce = L.x->view();
+    P.cbw = P.cb;
+    P.w = L.d_w;
+    P.visit_cap = 1;
+    ISMG_CUDA(cudaMalloc(&e->d_log, sizeof(int) * 2));
+    P.visit_log = e->d_log;
+    ISMG_CUDA(cudaMalloc(&e->d_ctl, sizeof(Ctl)));
+    ISMG_CUDA(cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
+    P.ctl = e->d_ctl;
+    ISMG_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
+    plan_coarse(*e, L.h, s.ctx->device);
+    return e;
+}
+
+// One visit: GS sweeps of the level until its residual is <= tol_coarse or the
+// budget (max_total_sweeps - total) is spent, from x = 0, anchored once when
+// singular; rc0 = the entry residual max|b|. Returns the sweeps; *rc the residual.
+long long coarse_engine_visit(FusedEngine& e, long long total, double rc0, int pred, double* rc) {
+    Ctx& c = *e.s->ctx;
+    Ctl init{};
+    init.phase = kCoarse;
+    init.rc = rc0;
+    init.pred = pred;
+    init.total = total;
+    init.nvisits = 1;
+    *e.h_ctl = init;
+    ISMG_CUDA(cudaMemcpyAsync(e.d_ctl, e.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c.stream));
+    launch_coarse(e, e.P, c.stream);
+    c.launches += e.cl_hybrid ? 2 : 1;
+    ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
+    ISMG_CUDA(cudaEventSynchronize(e.ev));
+    if (e.h_ctl->mp_error == 2) fail(ISMG_ERR_INTERNAL, "coarse visit: watchdog (mailbox / barrier timeout)");
+    *rc = e.h_ctl->rc;
+    return e.h_ctl->coarse;
 }
 
 FusedEngine* make_fused(Solver& s) {
@@ -244,49 +405,7 @@ FusedEngine* make_fused(Solver& s) {
         set_fine_pass_smem(e->smem);
     }
     ISMG_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
-    // coarse-visit kernel: TMEM-resident rhs when the operator allows it,
-    // else shared-memory iterate, else the global-memory wavefront
-    std::vector<double> spec;
-    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "rw" | "cl" | "tmem" | "smem" | "global"
-    const bool allow_rw = !force || std::string(force) == "rw";
-    const bool allow_cl = !force || std::string(force) == "cl";
-    const bool allow_tmem = !force || std::string(force) == "tmem";
-    const bool allow_smem = !force || std::string(force) == "smem" || std::string(force) == "tmem";
-    if (allow_rw && (e->rw = rw_try_create(L.h, c.device)) != nullptr) {
-        e->coarse_kind = 4;
-    } else if (allow_cl && cl_coarse_plan(L.h, e->cl, spec, e->coarse_smem)) {
-        e->coarse_kind = 3;
-        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
-        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
-        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * cl_backup_doubles(e->cl)));
-        size_t smax = e->coarse_smem;
-        // hybrid when the grid also fits one SM and the cluster is 2 SMs: a 2048^2
-        // step 1 takes 170 ms with it against 181 without; at 4096^2 (4 SMs) the
-        // one-SM kernel's shorter small groups are eaten by the extra launch per
-        // slot (494 against 487 ms). ISMG_CL_HYBRID=0 / 1 forces it off / on.
-        const char* hy = getenv("ISMG_CL_HYBRID");
-        const bool want = hy ? std::string(hy) != "0" : e->cl.csize == 2;
-        std::vector<double> spec1;
-        if (e->cl.csize > 1 && want &&
-            cl_coarse_plan(L.h, e->cl1, spec1, e->coarse_smem1, 128) && e->cl1.csize == 1 && spec1 == spec) {
-            e->cl_hybrid = true;
-            e->cl1.role = 1, e->cl.role = 2;
-            ISMG_CUDA(cudaMalloc(&e->coarse_backup1, sizeof(double) * cl_backup_doubles(e->cl1)));
-            smax = std::max(smax, e->coarse_smem1);
-        }
-        set_coarse_cl_smem(smax);
-    } else if (allow_tmem && tmem_coarse_plan(L.h, e->tm, spec, e->coarse_smem)) {
-        e->coarse_kind = 2;
-        ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
-        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
-        ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.pitch));
-        set_coarse_tmem_smem(e->coarse_smem);
-    } else if (allow_smem && size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double) <= 200 * 1024) {
-        e->coarse_kind = 1;
-        e->coarse_smem = size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double);
-        ISMG_CUDA(cudaMalloc(&e->coarse_backup, e->coarse_smem));
-        set_coarse_smem(e->coarse_smem);
-    }
+    plan_coarse(*e, L.h, c.device);
     (void)c;
     return e;
 }
@@ -295,6 +414,7 @@ void destroy_fused(FusedEngine* e) {
     if (!e) return;
     for (auto& ge : e->graphs)
         if (ge) cudaGraphExecDestroy(ge);
+    if (e->cond_exec) cudaGraphExecDestroy(e->cond_exec);
     e->scratch.free();
     cudaFree(e->P.part);
     cudaFree(e->P.ticket);
@@ -388,18 +508,7 @@ double fused_bench_coarse_visit(Solver& s, const Field& cb, Field& ce, long long
     ISMG_CUDA(cudaEventCreate(&e0));
     ISMG_CUDA(cudaEventCreate(&e1));
     ISMG_CUDA(cudaEventRecord(e0, c.stream));
-    if (e.coarse_kind == 4) {
-        launch_coarse_rw(e.P, *e.rw, c.stream);
-    } else if (e.coarse_kind == 3) {
-        if (e.cl_hybrid) launch_coarse_cl(e.P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, c.stream);
-        launch_coarse_cl(e.P, e.cl, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-    } else if (e.coarse_kind == 2) {
-        launch_coarse_tmem(e.P, e.tm, e.tm_spec, e.coarse_backup, e.coarse_smem, c.stream);
-    } else if (e.coarse_kind == 1) {
-        launch_coarse_smem(e.P, e.coarse_backup, e.coarse_smem, c.stream);
-    } else {
-        launch_coarse_global(e.P, c.stream);
-    }
+    launch_coarse(e, e.P, c.stream);
     ISMG_CUDA(cudaEventRecord(e1, c.stream));
     ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
     ISMG_CUDA(cudaMemcpy2DAsync(ce.buf.origin(), sizeof(double) * ce.buf.pitch, L.x->buf.origin(),
@@ -456,11 +565,28 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
         comm_reduce_scalars(*c.comm, e.bar_scratch, 1, 0, c.stream);
         c.comm->collectives += 1;
     }
-    // launch batches of [coarse-visit, fine-pass] slots until the phase is done
-    int slots = 8;
+    if (!e.P.mp && e.cond_state == 0) {
+        // ISMG_COND_GRAPH=1: the conditional graph. Off by default: measured A/B on one
+        // box (tools/visit_hist.py), the slot graphs' no-op launches cost less than the
+        // conditional nodes' per-iteration overhead: 4096^2 steps 1-3 449 / 239 / 251 ms
+        // against 456 / 245 / 257; 16384^2 3235 / 2385 / 3057 against 3321 / 2391 / 3062.
+        const char* cg = getenv("ISMG_COND_GRAPH");
+        e.cond_state = (cg && cg[0] == '1') ? (build_cond_graph(e) ? 1 : -1) : -1;
+    }
     long long launched_slots = 0;
+    if (e.cond_state == 1) {  // the whole solve: one graph launch, one wait
+        ISMG_CUDA(cudaGraphLaunch(e.cond_exec, c.stream));
+        ISMG_CUDA(cudaMemcpyAsync(e.h_ctl, e.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+        ISMG_CUDA(cudaEventRecord(e.ev, c.stream));
+        ISMG_CUDA(cudaEventSynchronize(e.ev));
+        s.last.host_syncs += 1;
+        if (e.h_ctl->phase != kDone) fail(ISMG_ERR_INTERNAL, "fused solve: conditional graph ended before the solve");
+        c.launches += e.h_ctl->passes + e.h_ctl->coarse_launches * (e.cl_hybrid ? 2 : 1);
+    }
+    // else: batches of [coarse-visit, fine-pass] slots until the phase is done
+    int slots = 8;
     int since_poll = 0;
-    for (;;) {
+    for (; e.cond_state != 1;) {
         ISMG_CUDA(cudaGraphLaunch(graph_for(e, slots), c.stream));
         c.launches += (1 + e.fine_launches + (e.P.mp ? 1 : 0)) * slots + (e.cl_hybrid ? slots : 0);
         launched_slots += slots;
@@ -514,7 +640,8 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.coarse_engine = e.coarse_kind;
     s.last.collectives = c.comm ? c.comm->collectives : 0;
     s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
-    s.last.kernel_launches = ((e.P.mp ? 3 : 2) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;
+    s.last.kernel_launches = e.cond_state == 1 ? st.passes + st.coarse_launches * (e.cl_hybrid ? 2 : 1) + 2
+                                               : ((e.P.mp ? 3 : 2) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;
 }
 
 }  // namespace ismgb

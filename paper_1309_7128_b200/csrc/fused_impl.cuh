@@ -86,7 +86,20 @@ struct Params {
     int64_t cb_off, cb_pitch;  // pack offset of coarse cell (I, J): cb_off + J * cb_pitch + I
     int64_t h_off[2];          // pack offsets of the first / last 3 rows
     View cbw;                  // single GPU: where the fused pass writes its tile sums (= cb)
+    // conditional CUDA graph of the single-GPU solve (fused_host.cu): WHILE(phase
+    // != done) { SWITCH(phase) { fine pass | coarse visit | prolong | resid } };
+    // the kernel that decides the next phase sets both conditions
+    int cond;
+    cudaGraphConditionalHandle h_while, h_switch;
 };
+
+// the next phase to the solve's conditional graph (no-op outside it)
+__device__ __forceinline__ void publish_phase(const Params& P, int phase) {
+    if (P.cond) {
+        cudaGraphSetConditional(P.h_switch, unsigned(phase));
+        cudaGraphSetConditional(P.h_while, phase != kDone ? 1u : 0u);
+    }
+}
 
 // x-row source of the fused passes: the rank's own rows from the field, the
 // neighbours' rows from their packs of the previous pass (parity hp)
@@ -191,7 +204,13 @@ __device__ __forceinline__ double group_sum(double v, int g) {
 }
 
 // ---- per-CTA epilogue + control flow (last CTA) ------------------------------
+__device__ __forceinline__ void fine_decide_(const Params& P, int mode, double r, double sum, double rc0);
+// cycles.hpp:111-161 on the pass's reductions; then the next phase to the graph
 __device__ __forceinline__ void fine_decide(const Params& P, int mode, double r, double sum, double rc0) {
+    fine_decide_(P, mode, r, sum, rc0);
+    publish_phase(P, P.ctl->phase);
+}
+__device__ __forceinline__ void fine_decide_(const Params& P, int mode, double r, double sum, double rc0) {
     Ctl* s = P.ctl;
     s->passes += 1;
     s->r = r;
@@ -301,7 +320,8 @@ size_t fine_pass_w_smem();
 void set_fine_pass_w_smem();
 dim3 fine_pass_w_grid(const Params& P);
 // kernels launched: single-GPU, the prolongation kernel then the sweep kernel (sweep_only: the sweep)
-int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only = false);
+// (sweep_only: the sweep kernel alone; ph2_only: the prolongation / residual kernel alone)
+int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only = false, bool ph2_only = false);
 void launch_finalize(const Params& P, View xuser, cudaStream_t st);
 void launch_mp_unpack(const Params& P, cudaStream_t st);
 void launch_coarse_global(const Params& P, cudaStream_t st);

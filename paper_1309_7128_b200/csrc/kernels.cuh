@@ -40,6 +40,29 @@ __device__ __forceinline__ double div_by_diag(double num, double d) {
     return __ddiv_rn(num, d);
 }
 
+// Correctly rounded num / w with y = RN(1 / w), no DDIV sequence. Two Markstein
+// corrections: q0 = RN(num y) is within 1.5 ulp of num / w; q1 = RN(q0 + RN(num -
+// w q0) y) is within one ulp (the residual's rounding error is 2^-53 relative);
+// by Markstein's theorem (y within half an ulp of 1/w, q1 within one ulp of
+// num/w, r1 = num - w q1 exact by FMA) q2 = RN(q1 + r1 y) = RN(num / w). The
+// theorem needs the residuals clear of underflow / overflow: numerators outside
+// [2^-900, 2^1000] (zero and subnormal-adjacent included) and non-finite ones
+// take IEEE division on a warp-uniform branch. Used by every coarse engine.
+static __device__ __noinline__ double div_ieee_lanes(double num, double w, double q, bool bad) {
+    return bad ? __ddiv_rn(num, w) : q;
+}
+__device__ __forceinline__ double div_cr(double num, double w, double y) {
+    const unsigned e = unsigned(__double2hiint(num)) & 0x7ff00000u;
+    const bool bad = e - (123u << 20) > (1900u << 20);
+    const double q0 = __dmul_rn(num, y);
+    const double e0 = __fma_rn(-q0, w, num);
+    const double q1 = __fma_rn(e0, y, q0);
+    const double e1 = __fma_rn(-q1, w, num);
+    double q = __fma_rn(e1, y, q1);
+    if (__any_sync(__activemask(), bad)) q = div_ieee_lanes(num, w, q, bad);
+    return q;
+}
+
 // std::max(m, v) with the reference's NaN behaviour: a NaN v is dropped.
 __device__ __forceinline__ double max_drop_nan(double m, double v) { return (m < v) ? v : m; }
 

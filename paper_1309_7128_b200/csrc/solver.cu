@@ -8,6 +8,7 @@
 //  * the op-level path below, which replays cycles.hpp's control flow on the
 //    host one reference call at a time (plain GS, the ACM V-cycle, and
 //    configurations the fused kernels do not cover).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -69,6 +70,12 @@ Solver::Solver(Ctx* c, const ismg_grid_spec& g0, const ismg_cycle_config& cfg0) 
     for (auto& L : levels) L.upload(*ctx, 0, 0);
     res = std::make_unique<Field>(ctx, g.nx, g.ny);
     if (fused_supported(*this)) fused = make_fused(*this);
+    if (cfg.scheme == ISMG_SCHEME_ACM && !levels.empty() && !levels.back().h.px && !levels.back().h.py) {
+        bool ok = true;  // a zero diagonal raises on the op-level path (coarsening.hpp:563-564)
+        const CoarseOpH& h = levels.back().h;
+        for (size_t k = 0; k < size_t(h.ncx) * h.ncy && ok; ++k) ok = h.w[k] != 0.0;
+        if (ok) acm_coarse = make_coarse_engine(*this, levels.back());
+    }
 }
 
 Solver::~Solver() {
@@ -76,6 +83,8 @@ Solver::~Solver() {
     cudaStreamSynchronize(ctx->stream);  // no throw from a destructor (the context may be torn down at exit)
     destroy_fused(fused);
     fused = nullptr;
+    destroy_fused(acm_coarse);
+    acm_coarse = nullptr;
     for (auto& L : levels) L.release();
 }
 
@@ -257,6 +266,7 @@ void Solver::solve_acm(Field& x, const Field& b, ismg_report& rep, Metrics& M) {
     const int64_t cells = int64_t(g.nx) * g.ny;
     k_zero_ghosts(*ctx, x.view());
     long total = 0;
+    int acm_pred = 1;  // first sweep group of the next coarsest visit (the last visit's length)
     double r = fine_residual(x, b, res.get(), true);
     anchor_mean(x);
     auto check_diag = [&](const LevelDev& lv) {
@@ -294,6 +304,25 @@ void Solver::solve_acm(Field& x, const Field& b, ismg_report& rep, Metrics& M) {
                     ++total;
                 }
                 coarse_residual(lv, *lv.x, *lv.b, lv.r.get(), false);
+            } else if (acm_coarse && mode == 0) {
+                // the coarsest level's GS loop (cycles.hpp:222-235) as ONE device-resident
+                // coarse visit (the fused path's coarse kernel): one launch, one wait
+                const double rc = coarse_residual(lv, *lv.x, *lv.b, nullptr, true);  // x = 0: max|b|
+                if (rc > cfg.tol_coarse) {
+                    if (total >= cfg.max_total_sweeps) {
+                        capped = true;
+                    } else {
+                        double rc_end = 0.0;
+                        const long long n = coarse_engine_visit(*acm_coarse, total, rc, acm_pred, &rc_end);
+                        last.host_syncs += 1;
+                        last.coarse_visits += 1;
+                        for (long long q = 0; q < n; ++q) M.sweep(false, 5, int64_t(lv.h.ncx) * lv.h.ncy);
+                        rep.coarse_sweeps += n;
+                        total += long(n);
+                        if (n > 0) acm_pred = int(std::min<long long>(n, 1 << 20));
+                        if (rc_end > cfg.tol_coarse) capped = true;  // the budget ran out first
+                    }
+                }
             } else {
                 double rc = coarse_residual(lv, *lv.x, *lv.b, nullptr, true);
                 while (rc > cfg.tol_coarse) {

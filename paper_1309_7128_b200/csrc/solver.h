@@ -52,6 +52,7 @@ struct Solver {
     std::vector<LevelDev> levels;  // ISMG/GMG: one; ACM: depth-1 (finest first)
     std::unique_ptr<Field> res;    // residual scratch of the op-level paths
     FusedEngine* fused = nullptr;
+    FusedEngine* acm_coarse = nullptr;  // ACM: coarse-visit engine of the coarsest level (device-resident loop)
     ismg_solve_stats last{};
     std::vector<int> visit_log;  // (coarse sweeps, fine sweeps) per outer iteration of the last solve
     int mode = 0;  // 0 = auto (fused hot path when supported), 1 = op-level reference order
@@ -95,6 +96,8 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
                  double** pending_shift);
 void destroy_fused(FusedEngine* e);
 double fused_bench_fine_pass(Solver& s, Field& x, const Field& b, int iters);
+FusedEngine* make_coarse_engine(Solver& s, LevelDev& L);
+long long coarse_engine_visit(FusedEngine& e, long long total, double rc0, int pred, double* rc);
 double fused_bench_coarse_visit(Solver& s, const Field& cb, Field& ce, long long budget, int first,
                                 long long* sweeps, double* rc);
 

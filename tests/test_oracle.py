@@ -526,3 +526,46 @@ def test_writers_match_the_reference_bytes(ref, tmp_path, which):
     api.write_operator_csv(ncx, ncy, w, mine[2])
     for a, b in zip(paths, mine):
         assert open(a, "rb").read() == open(b, "rb").read(), b
+
+
+def _fma(a, b, c):
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))  # one rounding (float(Fraction) is RN)
+
+
+def _div_cr(num, w, y):
+    """kernels.cuh div_cr restated: two Markstein corrections with y = RN(1/w)."""
+    q0 = num * y
+    q1 = _fma(_fma(-q0, w, num), y, q0)
+    return _fma(_fma(-q1, w, num), y, q1)
+
+
+def test_markstein_division_is_correctly_rounded():
+    """The coarse engines' division (kernels.cuh div_cr) equals IEEE num / w bit for
+    bit on the divisors the ISMG operators produce (-3 in the interior; ring and
+    Dirichlet-closure classes) and on random ones, for random numerators across the
+    guarded exponent range [2^-900, 2^1000] plus adversarial significands (all-ones,
+    powers of two, values next to multiples of w)."""
+    import math
+    import struct
+    rng = np.random.default_rng(1309)
+    divisors = [-3.0, -2.25, -2.5, -2.75, -3.5, -4.0, -1.75, -5.0, -6.0, -0.75, 3.0, -2.875, -3.125, -2.375]
+    divisors += [float(-rng.uniform(0.5, 8.0)) for _ in range(10)]
+    bad = 0
+    for w in divisors:
+        y = 1.0 / w
+        nums = []
+        for _ in range(1500):
+            m = rng.uniform(1.0, 2.0)
+            nums.append(math.ldexp(m, int(rng.integers(-899, 999))) * (1 if rng.random() < 0.5 else -1))
+        for e in (-899, -1, 0, 1, 52, 998):
+            for mant in (1.0, 2.0 - 2.0 ** -52, 1.0 + 2.0 ** -52, 1.5):
+                nums.append(math.ldexp(mant, e))
+        for k in range(1, 200):  # next to exact multiples: k*w and its neighbours
+            base = k * w * 1.000000001
+            nums += [base, math.nextafter(base, math.inf), math.nextafter(base, -math.inf)]
+        for n in nums:
+            got, want = _div_cr(n, w, y), n / w
+            if struct.pack("<d", got) != struct.pack("<d", want):
+                bad += 1
+    assert bad == 0
