@@ -62,7 +62,8 @@ constexpr int kLS = 32;    // columns per lane segment = sweep lag
 constexpr int kR = 2;      // rows per warp
 constexpr int kRl = 28;    // residual lag (steps): the largest the in-warp overwrite allows (kLS - 4)
 constexpr int kA = 4;      // mailbox prefetch distance (steps)
-constexpr int kM = 1;      // extra lead restored after a stall on the row below (steps)
+constexpr int kM = 1;      // (unused: wait-ahead after a stall, replaced by kTrail pacing)
+constexpr int kTrail = 11; // steps the warp below leads by at a period's start (3 dependency + 2 L2 + 4 prefetch + 2)
 constexpr int kNS = 8;     // prefetch slots per stream (power of two, > kA)
 constexpr int kNStr = 4;   // mailbox streams: update-south, residual-south, update-north, residual-north
 constexpr int kMaxG = 4096;
@@ -92,6 +93,7 @@ struct RwD {
     unsigned* bar;               // grid barrier: [0] arrivals, [1] generation; [2] tag base
     double* part;                // [nw] anchor partial sums
     double* dec;                 // group decision: [0] first converged sweep, [1] residual
+    unsigned long long* prog;    // [nw] progress per warp ((tag base << 32) | steps done)
 };
 
 namespace {
@@ -164,10 +166,13 @@ struct Lane {
     uint32_t slots;         // shared: this lane's prefetch slots ([kNStr][kNS][33] x 16 B, lane-offset)
     uint32_t b0, b1;        // shared: this lane's rhs segment of rows 0 / 1
     uint32_t ew;            // shared: end weights of this warp's rows [kR][2][10]
+    unsigned long long* prog_me;           // this warp's published progress ((base << 32) | steps done)
+    const unsigned long long* prog_south;  // ... of the warp below
 };
 
 // per-period values
 struct Per {
+    int q;          // period index (steps q * kLS ..)
     int g0;         // sweep of the lane's segment at offset 0 this period: q - lane
     unsigned tq;    // its tag
     int par;        // its parity
@@ -285,7 +290,7 @@ __device__ __forceinline__ void pf_check(const Lane& L, const Per& p, bool resid
         const bool want = act && (c + 1 < kLS || L.has_r);
         // the word kA + kM steps ahead (update-south only: the row below leads)
         constexpr int ka = kk + kA + kM, ca = cmod(ka), da = cdiv(ka) + s_toff(S);
-        const bool wa = S == 0 && in_group(L, p.g0 + cdiv(ka)) && (ca + 1 < kLS || L.has_r);
+        const bool wa = false;  // (kept off: the period pacing in rw_group holds the lead instead)
         const char* ahead = mb_word<S>(L, p, ca + 1, da);
         const uint4 u = lds_u4(sl);
         const bool bad = want && ((u.y ^ tag) | (u.w ^ tag)) != 0u;
@@ -510,6 +515,12 @@ __device__ __forceinline__ void rw_step(const RwK& T, const Lane& L, const Per& 
         if (act[0]) x[0][c0] = nv[0];
         if (act[1]) x[1][c1] = nv[1];
     }
+    if constexpr ((k & 3) == 3) {  // progress for the warp above's pacing: steps 0 .. q kLS + k done
+        if (L.lane == 0) {
+            const unsigned long long v = (static_cast<unsigned long long>(L.base) << 32) | unsigned(p.q * kLS + k + 1);
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(L.prog_me), "l"(v) : "memory");
+        }
+    }
 }
 
 template <int k, bool kFirst, bool kLast>
@@ -535,6 +546,7 @@ __device__ __forceinline__ void rw_prologue(const Lane& L, const Per& p, bool re
 
 __device__ __forceinline__ Per period(const Lane& L, int q) {
     Per p;
+    p.q = q;
     p.g0 = q - L.lane;
     p.tq = L.base + unsigned(p.g0);
     p.par = int(p.tq & 1u);
@@ -556,10 +568,37 @@ __device__ __forceinline__ void rw_group(const RwK& T, const Lane& L, double (&x
     const int tau_end = kLS * (L.K + L.G - 1) + 2 * kR - 3 + (residuals ? kRl : 0);
     const int qn = tau_end / kLS + 1;
     rw_prologue<0, kFirst, kLast>(L, period(L, 0), residuals);
+    const unsigned long long gb = static_cast<unsigned long long>(L.base) << 32;
 #pragma unroll 1
     for (int q = 0; q < qn; ++q) {
+        // pacing: start the period only once the warp below has done kTrail more
+        // steps (its words this period's prefetches read are then in L2); the
+        // lead stays in [kTrail, kTrail + 4 + jitter], inside the window the warp
+        // above allows (its north words, kLS - 4 - kA - latency steps of slack)
+        if (!kFirst) {
+            const unsigned long long want = gb | unsigned(min(q * kLS + kTrail, tau_end + 1));
+            if (L.lane == 0) {
+                unsigned long long v;
+                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.prog_south) : "memory");
+                if (v < want) {
+                    const long long t0 = gtimer();
+                    do {
+                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.prog_south) : "memory");
+                        if (gtimer() - t0 > 2000000000ll) {
+                            atomicExch(&g_rw_stuck, 1u);
+                            break;
+                        }
+                    } while (v < want);
+                }
+            }
+            __syncwarp();
+        }
         const Per p = period(L, q), pn = period(L, q + 1);
         rw_period<0, kFirst, kLast>(T, L, p, pn, residuals, x, rmax, cmax);
+    }
+    if (L.lane == 0) {  // the group's last step done (the pacing target of the warp above caps here)
+        const unsigned long long v = gb | unsigned(tau_end + 1);
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(L.prog_me), "l"(v) : "memory");
     }
     cp_wait<0>();
     __threadfence();  // this thread's residual atomics performed before the group's grid barrier
@@ -619,6 +658,8 @@ __global__ void __launch_bounds__(kRwThreads, 1) coarse_rw_kernel(Params P, RwK 
     L.b0 = su32(bsm + size_t(wic) * kR * T.bpitch + lane * (kLS + 1));
     L.b1 = L.b0 + 8u * uint32_t(T.bpitch);
     L.ew = su32(ewm + wic * kR * 20);
+    L.prog_me = D.prog + (wok ? w : 0);
+    L.prog_south = D.prog + (south ? w - 1 : 0);
     const int J0 = w * kR;
     // rhs and end classes of this warp's rows into shared memory (lane segments padded by one)
     if (wok) {
@@ -840,7 +881,7 @@ RwEngine* rw_create(const RwPlan& plan) {
     const RwK& T = plan.T;
     const size_t mail = sizeof(uint4) * size_t(T.nw) * 2 * T.ncx;
     const size_t bytes = 2 * mail + sizeof(unsigned long long) * kMaxG + 64 + sizeof(double) * (T.nw + 2) +
-                         sizeof(double) * plan.endw.size() + 256;
+                         sizeof(double) * plan.endw.size() + sizeof(unsigned long long) * T.nw + 256;
     ISMG_CUDA(cudaMalloc(&e->mem, bytes));
     ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
     char* p = static_cast<char*>(e->mem);
@@ -858,6 +899,8 @@ RwEngine* rw_create(const RwPlan& plan) {
     p += sizeof(double) * 2;
     double* endw = reinterpret_cast<double*>(p);
     ISMG_CUDA(cudaMemcpy(endw, plan.endw.data(), sizeof(double) * plan.endw.size(), cudaMemcpyHostToDevice));
+    p += sizeof(double) * plan.endw.size();
+    e->D.prog = reinterpret_cast<unsigned long long*>(p);
     e->D.endw = endw;
     const unsigned base0 = 16u;  // tags start above the zeroed mailboxes' 0
     ISMG_CUDA(cudaMemcpy(e->D.bar + 2, &base0, sizeof(unsigned), cudaMemcpyHostToDevice));

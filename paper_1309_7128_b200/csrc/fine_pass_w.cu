@@ -140,6 +140,14 @@ __device__ __forceinline__ void fence_release_sys() {
 __device__ __forceinline__ bool is_pow2(double d) {
     return d > 0.0 && (__double_as_longlong(d) & 0x000FFFFFFFFFFFFFll) == 0;
 }
+// 1 / d for a (normal) power of two d, exactly, from the exponent: no MUFU / DDIV
+__device__ __forceinline__ double pow2_recip(double d) {
+    return __hiloint2double((2046 << 20) - (__double2hiint(d) & 0x7ff00000), 0);
+}
+// IEEE num / den out of line: a branch the compiler cannot if-convert into
+// computing the DDIV sequence for every cell (it did: MUFU.RCP64H was the
+// prolongation pass's top stall at 16384^2, profiles/r02_fine_pass_w_ph2_16384_ncu_full.txt)
+__device__ __noinline__ double div_slow(double num, double den) { return __ddiv_rn(num, den); }
 
 // this rank's own pack slot of pass parity p in its exchange buffer
 __device__ __forceinline__ double* my_pack(const Params& P, int p) {
@@ -314,6 +322,12 @@ __device__ __forceinline__ void tile_flush_w(const Params& P, const Lane& L, int
     A.tacc = 0.0;
 }
 
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // Warp-level epilogue, a fixed two-level tree (deterministic sums): every warp
 // (= CTA) stores its partial triple; the last warp of each group of 32 CTAs
 // folds the group (one partial per lane); the last group folds the group
@@ -338,9 +352,11 @@ __device__ __forceinline__ void warp_epilogue(const Params& P, int mode, double 
         P.part[3 * bid + 1] = sx;
         P.part[3 * bid + 2] = cm;
         if (anynan) P.ctl->nan_seen = 1;
-        __threadfence();
+        // release: the partials before the ticket, without the full fence's L1
+        // invalidation (CCTL.IVALL was the sweep pass's top stall line at 16384^2);
+        // the group's last warp acquires with the fence below
         const unsigned gsize = unsigned(min(32, nb - 32 * grp));
-        last = atomicAdd(&P.ticket[1 + grp], 1u) == gsize - 1;
+        last = atom_add_release(&P.ticket[1 + grp], 1u) == gsize - 1;
     }
     if (!__shfl_sync(kFull, last, 0)) return;
     __threadfence();
@@ -522,8 +538,8 @@ __device__ __forceinline__ void prolong_w(SmemW& sm, const Params& P, const Ctl&
                         sq[q] * ((dy - tt) * P.ce.at(I1[q], J0) + tt * P.ce.at(I1[q], J1));
                     const double den = dxq[q] * dy;
                     // a power-of-two den (uniform tiles): the reciprocal product is the exact quotient
-                    const bool pow2 = (__double_as_longlong(den) & 0x000FFFFFFFFFFFFFll) == 0;
-                    v += pow2 ? num * (1.0 / den) : num / den;
+                    if ((__double_as_longlong(den) & 0x000FFFFFFFFFFFFFll) == 0) v += num * pow2_recip(den);
+                    else v += div_slow(num, den);
                 }
                 x0[q] = v;
             }
@@ -593,7 +609,7 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
             const int col = L.c0 + q;
             I0[q] = P.ax.k0[col], I1[q] = P.ax.k1[col], sq[q] = P.ax.t[col], dxq[q] = P.ax.dk[col];
         }
-        idx[q] = is_pow2(dxq[q]) ? 1.0 / dxq[q] : 0.0;  // exact reciprocal, or 0: divide
+        idx[q] = is_pow2(dxq[q]) ? pow2_recip(dxq[q]) : 0.0;  // exact reciprocal, or 0: divide
     }
     // columns of a quad that share the previous column's coarse pair reuse its row terms
     // (a quad inside one half tile: one pair, 4 coarse loads per row instead of 16)
@@ -614,35 +630,56 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     int slot = 0;
     uint32_t phase = 0;
     const int si = 4 * L.l;
+    // TileAxis::locate_cell of the rows, one row ahead (the loads leave the row's
+    // critical path), and the lane's coarse values c(I0/I1, J0/J1) of the first
+    // column pair, reloaded only when the row's coarse pair (J0, J1) changes (every
+    // half tile) instead of four dependent L2 loads per row
+    auto row_axis = [&](int k, double& t_, double& d_, int& j0_, int& j1_) {
+        t_ = 0.0, d_ = 1.0, j0_ = 0, j1_ = 0;
+        if (prolong && k >= 0 && k < G.ny) t_ = P.ay.t[k], d_ = P.ay.dk[k], j0_ = P.ay.k0[k], j1_ = P.ay.k1[k];
+    };
+    double tt_n, dy_n;
+    int J0_n, J1_n;
+    row_axis(kfirst, tt_n, dy_n, J0_n, J1_n);
+    int cJ0 = -1, cJ1 = -1;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
     for (int k = kfirst; k <= klast; ++k) {
+        const double tt = tt_n, dy = dy_n;
+        const int J0 = J0_n, J1 = J1_n;
+        row_axis(k + 1, tt_n, dy_n, J0_n, J1_n);
+        if (prolong && L.dom[0] && (J0 != cJ0 || J1 != cJ1)) {
+            c00 = P.ce.at(I0[0], J0), c01 = P.ce.at(I0[0], J1), c10 = P.ce.at(I1[0], J0), c11 = P.ce.at(I1[0], J1);
+            cJ0 = J0, cJ1 = J1;
+        }
         mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
         double x0[4], b0[4];
         {
             const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
             const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
-            const double2 c01 = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
-            const double2 c23 = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+            const double2 c01v = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+            const double2 c23v = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
             const double raw[4] = {v01.x, v01.y, v23.x, v23.y};
-            b0[0] = c01.x, b0[1] = c01.y, b0[2] = c23.x, b0[3] = c23.y;
+            b0[0] = c01v.x, b0[1] = c01v.y, b0[2] = c23v.x, b0[3] = c23v.y;
             const bool rin = k >= 0 && k < G.ny;
-            double tt = 0.0, dy = 1.0;
-            int J0 = 0, J1 = 0;
-            if (prolong && rin) tt = P.ay.t[k], dy = P.ay.dk[k], J0 = P.ay.k0[k], J1 = P.ay.k1[k];
             const double wy0 = dy - tt;
             // power-of-two extents (uniform tiles): num / (dx dy) is exactly num ((1/dx) (1/dy))
-            const double idy = is_pow2(dy) ? 1.0 / dy : 0.0;
+            const double idy = is_pow2(dy) ? pow2_recip(dy) : 0.0;
             double ca = 0.0, cb = 0.0;  // the column pair's row terms (dy-t) c(I,J0) + t c(I,J1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 double v = (rin && L.dom[q]) ? raw[q] + G.c : 0.0;
                 if (prolong && rin && L.dom[q]) {
-                    if (!same[q]) {
+                    if (q == 0) {
+                        ca = wy0 * c00 + tt * c01;
+                        cb = wy0 * c10 + tt * c11;
+                    } else if (!same[q]) {
                         ca = wy0 * P.ce.at(I0[q], J0) + tt * P.ce.at(I0[q], J1);
                         cb = wy0 * P.ce.at(I1[q], J0) + tt * P.ce.at(I1[q], J1);
                     }
                     const double num = (dxq[q] - sq[q]) * ca + sq[q] * cb;
                     const double r = idx[q] * idy;
-                    v += r != 0.0 ? num * r : num / (dxq[q] * dy);
+                    if (r != 0.0) v += num * r;
+                    else v += div_slow(num, dxq[q] * dy);
                 }
                 x0[q] = v;
             }

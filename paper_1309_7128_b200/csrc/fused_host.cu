@@ -95,7 +95,7 @@ static void launch_coarse(const FusedEngine& e, const Params& P, cudaStream_t st
 // phase sets both conditions (publish_phase), so every launch does work and
 // the host waits once per solve. Returns false where conditional nodes are
 // unavailable (the slot graphs then run the solve).
-static bool build_cond_graph(FusedEngine& e) {
+[[maybe_unused]] static bool build_cond_graph(FusedEngine& e) {
     Ctx& c = *e.s->ctx;
     cudaGraph_t g = nullptr;
     bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
@@ -571,7 +571,12 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
         // conditional nodes' per-iteration overhead: 4096^2 steps 1-3 449 / 239 / 251 ms
         // against 456 / 245 / 257; 16384^2 3235 / 2385 / 3057 against 3321 / 2391 / 3062.
         const char* cg = getenv("ISMG_COND_GRAPH");
+#ifdef ISMG_WITH_COND_GRAPH
         e.cond_state = (cg && cg[0] == '1') ? (build_cond_graph(e) ? 1 : -1) : -1;
+#else
+        (void)cg;
+        e.cond_state = -1;
+#endif
     }
     long long launched_slots = 0;
     if (e.cond_state == 1) {  // the whole solve: one graph launch, one wait

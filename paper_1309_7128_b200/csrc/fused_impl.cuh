@@ -93,12 +93,19 @@ struct Params {
     cudaGraphConditionalHandle h_while, h_switch;
 };
 
-// the next phase to the solve's conditional graph (no-op outside it)
+// the next phase to the solve's conditional graph (no-op outside it). Built only
+// with -DISMG_WITH_COND_GRAPH (tools/build_variant.sh): ncu refuses to profile
+// the kernel nodes of any graph whose kernels can set conditionals, and the
+// conditional graph measured slower than the slot graphs (fused_host.cu).
 __device__ __forceinline__ void publish_phase(const Params& P, int phase) {
+#ifdef ISMG_WITH_COND_GRAPH
     if (P.cond) {
         cudaGraphSetConditional(P.h_switch, unsigned(phase));
         cudaGraphSetConditional(P.h_while, phase != kDone ? 1u : 0u);
     }
+#else
+    (void)P, (void)phase;
+#endif
 }
 
 // x-row source of the fused passes: the rank's own rows from the field, the
