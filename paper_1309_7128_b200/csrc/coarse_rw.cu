@@ -246,7 +246,9 @@ __device__ __forceinline__ bool ll_wait(const char* word, unsigned tag, long lon
 
 __device__ double g_rw_trace[8192];
 __device__ unsigned g_rw_trace_n;
-__device__ unsigned long long g_rw_slow[6];  // debug counters: slow-path entries by stream [0..3], own-column words [4], waits ahead [5]
+__device__ unsigned long long g_rw_slow[6];
+// debug (ISMG_RW_TRACE): per warp [group cycles, slow-path cycles, pacing-spin cycles] of the last group
+__device__ unsigned long long g_rw_cyc[3 * 1024];  // debug counters: slow-path entries by stream [0..3], own-column words [4], waits ahead [5]
 
 // Slow path (warp-uniform): re-read a stale mailbox word until the writer's tag
 // shows and put it back into its slot (read again by later steps / the lane
@@ -257,11 +259,16 @@ __device__ unsigned long long g_rw_slow[6];  // debug counters: slow-path entrie
 __device__ __noinline__ void ll_settle(uint32_t slot, const char* word, unsigned tag, bool bad, const char* ahead,
                                        unsigned tag_ahead, bool wait_ahead, int stream) {
     const long long t0 = gtimer();
+#ifdef ISMG_RW_COUNTERS
+    const long long c0 = clock64();
     const bool any_wa = __any_sync(kFull, wait_ahead);
     if (threadIdx.x % 32 == 0) {
         atomicAdd(&g_rw_slow[stream], 1ull);
         if (any_wa) atomicAdd(&g_rw_slow[5], 1ull);
     }
+#else
+    (void)stream;
+#endif
     if (bad) {
         uint4 u;
         for (;;) {
@@ -276,6 +283,10 @@ __device__ __noinline__ void ll_settle(uint32_t slot, const char* word, unsigned
     }
     if (wait_ahead) ll_wait(ahead, tag_ahead, t0);
     __syncwarp();
+#ifdef ISMG_RW_COUNTERS
+    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && wg < 1024) atomicAdd(&g_rw_cyc[3 * wg + 1], (unsigned long long)(clock64() - c0));
+#endif
 }
 
 // validate the words delivered to stream S's slots at (static) step k
@@ -569,6 +580,12 @@ __device__ __forceinline__ void rw_group(const RwK& T, const Lane& L, double (&x
     const int qn = tau_end / kLS + 1;
     rw_prologue<0, kFirst, kLast>(L, period(L, 0), residuals);
     const unsigned long long gb = static_cast<unsigned long long>(L.base) << 32;
+    const long long cg0 = clock64();
+    if (L.lane == 0) {
+        const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (wg < 1024) g_rw_cyc[3 * wg + 1] = 0, g_rw_cyc[3 * wg + 2] = 0;
+    }
+    __syncwarp();
 #pragma unroll 1
     for (int q = 0; q < qn; ++q) {
         // pacing: start the period only once the warp below has done kTrail more
@@ -582,6 +599,7 @@ __device__ __forceinline__ void rw_group(const RwK& T, const Lane& L, double (&x
                 asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.prog_south) : "memory");
                 if (v < want) {
                     const long long t0 = gtimer();
+                    const long long c0 = clock64();
                     do {
                         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.prog_south) : "memory");
                         if (gtimer() - t0 > 2000000000ll) {
@@ -589,6 +607,8 @@ __device__ __forceinline__ void rw_group(const RwK& T, const Lane& L, double (&x
                             break;
                         }
                     } while (v < want);
+                    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                    if (wg < 1024) g_rw_cyc[3 * wg + 2] += (unsigned long long)(clock64() - c0);
                 }
             }
             __syncwarp();
@@ -599,6 +619,8 @@ __device__ __forceinline__ void rw_group(const RwK& T, const Lane& L, double (&x
     if (L.lane == 0) {  // the group's last step done (the pacing target of the warp above caps here)
         const unsigned long long v = gb | unsigned(tau_end + 1);
         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(L.prog_me), "l"(v) : "memory");
+        const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (wg < 1024) g_rw_cyc[3 * wg] = (unsigned long long)(clock64() - cg0);
     }
     cp_wait<0>();
     __threadfence();  // this thread's residual atomics performed before the group's grid barrier
@@ -919,6 +941,12 @@ std::vector<double> rw_trace_take() {
     ISMG_CUDA(cudaMemcpyFromSymbol(slow, g_rw_slow, sizeof(slow)));
     v.push_back(-2.0);
     for (unsigned long long c : slow) v.push_back(double(c));
+    std::vector<unsigned long long> cyc(3 * 1024);
+    ISMG_CUDA(cudaMemcpyFromSymbol(cyc.data(), g_rw_cyc, sizeof(unsigned long long) * cyc.size()));
+    for (int w : {0, 1, 2, 3, 4, 5, 64, 127, 128, 200, 255}) {
+        v.push_back(-3.0), v.push_back(double(w));
+        for (int k = 0; k < 3; ++k) v.push_back(double(cyc[3 * w + k]));
+    }
     const unsigned long long z2[6] = {0, 0, 0, 0, 0, 0};
     ISMG_CUDA(cudaMemcpyToSymbol(g_rw_slow, z2, sizeof(z2)));
     return v;

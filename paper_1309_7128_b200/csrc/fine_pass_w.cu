@@ -40,7 +40,11 @@ namespace {
 #define ISMG_MP_FENCE_SC 0
 #endif
 #ifndef ISMG_FINE_MINB_PR
-#define ISMG_FINE_MINB_PR 14  // the prolongation / residual kernel
+// the prolongation / residual kernel: 12 resident warps (168 registers, no spill,
+// y-axis tables staged in shared memory). Same-box A/B (tools/visit_hist.py,
+// solve ms): 16384^2 step 1 3127 at 12 against 3351 at 16 and 3461 at 14 with the
+// staged tables; 4096^2 steps 1-3 437 / 232 / 245 against 458 / 245 / 257 at 14.
+#define ISMG_FINE_MINB_PR 12
 #endif
 #ifndef ISMG_FINE_MINB_MP
 #define ISMG_FINE_MINB_MP 1  // the multi-GPU variant spills at 14
@@ -634,9 +638,29 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     // critical path), and the lane's coarse values c(I0/I1, J0/J1) of the first
     // column pair, reloaded only when the row's coarse pair (J0, J1) changes (every
     // half tile) instead of four dependent L2 loads per row
+    // the chunk's rows of the y-axis tables, staged once into shared memory with
+    // coalesced loads (four dependent L2 loads per row were the pass's top stall)
+    constexpr int kAxRows = 100;
+    __shared__ double s_at[kAxRows], s_adk[kAxRows];
+    __shared__ int s_ak0[kAxRows], s_ak1[kAxRows];
+    const bool tab = prolong && klast - kfirst + 2 <= kAxRows;
+    if (tab) {
+        for (int i = int(threadIdx.x & 31); i < klast - kfirst + 2; i += 32) {
+            const int k = kfirst + i;
+            const bool in = k >= 0 && k < G.ny;
+            s_at[i] = in ? P.ay.t[k] : 0.0, s_adk[i] = in ? P.ay.dk[k] : 1.0;
+            s_ak0[i] = in ? P.ay.k0[k] : 0, s_ak1[i] = in ? P.ay.k1[k] : 0;
+        }
+        __syncwarp();
+    }
     auto row_axis = [&](int k, double& t_, double& d_, int& j0_, int& j1_) {
         t_ = 0.0, d_ = 1.0, j0_ = 0, j1_ = 0;
-        if (prolong && k >= 0 && k < G.ny) t_ = P.ay.t[k], d_ = P.ay.dk[k], j0_ = P.ay.k0[k], j1_ = P.ay.k1[k];
+        if (tab) {
+            const int i = k - kfirst;
+            t_ = s_at[i], d_ = s_adk[i], j0_ = s_ak0[i], j1_ = s_ak1[i];
+        } else if (prolong && k >= 0 && k < G.ny) {
+            t_ = P.ay.t[k], d_ = P.ay.dk[k], j0_ = P.ay.k0[k], j1_ = P.ay.k1[k];
+        }
     };
     double tt_n, dy_n;
     int J0_n, J1_n;

@@ -522,7 +522,8 @@ double fused_bench_coarse_visit(Solver& s, const Field& cb, Field& ce, long long
     if (e.h_ctl->mp_error == 2) fail(ISMG_ERR_INTERNAL, "coarse visit: watchdog (mailbox / barrier timeout)");
     if (e.coarse_kind == 4 && getenv("ISMG_RW_TRACE")) {  // debug: per-group residual maxima to stderr
         const std::vector<double> t = rw_trace_take();
-        for (double v : t) fprintf(stderr, v == -1.0 ? "\nRWTRACE" : (v == -2.0 ? "\nRWSLOW" : " %.17g"), v);
+        for (double v : t)
+            fprintf(stderr, v == -1.0 ? "\nRWTRACE" : (v == -2.0 ? "\nRWSLOW" : (v == -3.0 ? "\nRWCYC" : " %.17g")), v);
         fprintf(stderr, "\n");
     }
     *sweeps = e.h_ctl->coarse;
