@@ -52,7 +52,10 @@ constexpr int kHandG = 4;          // role 1: largest group run on one SM
 #define ISMG_CL_S4 3  // barrier interval on a 4-SM cluster (tuning hook)
 #endif
 #ifndef ISMG_CL_S8
-#define ISMG_CL_S8 4  // ... on 8 or more SMs
+// ... on 8 or more SMs. Same-box A/B at 16384^2 (coarse 512^2, 16 SMs; tools/
+// visit_hist.py, coarse ms of steps 1-3): S = 8 1702 / 663 / 785 against 1790 /
+// 701 / 829 at S = 4, 1862 / 693 / 817 at 6, 1794 / 678 / 800 at 12.
+#define ISMG_CL_S8 8
 #endif
 constexpr int kIntWarps = 16;     // warps: 4 row blocks x 4 sweeps in flight
 constexpr int kClThreads = 32 * kIntWarps;
