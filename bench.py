@@ -513,7 +513,8 @@ def main():
     if world > 1 and "RANK" in os.environ:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local_rank)
+        if args.impl == "ours":  # the reference arm is CPU-only (gloo), no device needed
+            torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)

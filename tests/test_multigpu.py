@@ -87,3 +87,25 @@ def test_two_gpu_strips_match_single_gpu():
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
         assert r.stdout.count('"ok": true') == 2
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """bench.py's launch contract at N = 2 on CPU (gloo): `--impl reference` under torchrun
+    prints exactly one JSON line, from rank 0, with the reference arm's keys; rank 1 exits 0
+    without work. The workload is config 1 (lid 256^2), whose per-step counts come from the
+    reference's own fixture."""
+    import json
+    import random
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29700 + random.randrange(200)),
+                        os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--grid", "256",
+                        "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 2
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and "lid-driven cavity 256x256" in d["config"]["workload"]
