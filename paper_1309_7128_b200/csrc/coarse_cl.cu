@@ -57,7 +57,10 @@ constexpr int kHandG = 4;          // role 1: largest group run on one SM
 // 701 / 829 at S = 4, 1862 / 693 / 817 at 6, 1794 / 678 / 800 at 12.
 #define ISMG_CL_S8 8
 #endif
-constexpr int kIntWarps = 16;     // warps: 4 row blocks x 4 sweeps in flight
+#ifndef ISMG_CLX_WARPS
+#define ISMG_CLX_WARPS 16
+#endif
+constexpr int kIntWarps = ISMG_CLX_WARPS;  // warps: 4 row blocks x 4 sweeps in flight
 constexpr int kClThreads = 32 * kIntWarps;
 
 constexpr int kMaxRowBlocks = 4;  // 32-row blocks per CTA band
@@ -179,6 +182,9 @@ __device__ __forceinline__ double apply_lane(const Wts& W, const Nbr& v, double 
     const double num = bIJ - acc;
     if (kResidual) return num;
     if (!fastdiv) return num / W.w[0];
+#ifdef ISMG_CLX_NODIV
+    return num * W.y;
+#endif
     return div_cr(num, W.w[0], W.y);  // correctly rounded (kernels.cuh)
 }
 
@@ -297,8 +303,12 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
                 bu = cl_dyn[browo + Iuc];
                 br_ = cl_dyn[browo + Irc];
             } else {
+#ifdef ISMG_CLX_NOB
+                bu = 0.5, br_ = 0.25;
+#else
                 bu = __ldg(brow + Iuc);
                 br_ = __ldg(brow + Irc);
+#endif
             }
             // both cells, branch-free, so their independent fp64 chains interleave
             const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
@@ -340,7 +350,11 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
             } else if constexpr (BM == 1) {
                 bu = cl_dyn[browo + Iuc];
             } else {
+#ifdef ISMG_CLX_NOB
+                bu = 0.5;
+#else
                 bu = __ldg(brow + Iuc);
+#endif
             }
             const Nbr vu = gather(rowo + Iuc, pitch, false, kFive);
             const double out = apply_lane<false, kFive, kSel>(Wu, vu, bu, fastdiv);
@@ -367,7 +381,11 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
             } else if constexpr (BM == 1) {
                 br_ = cl_dyn[browo + Irc];
             } else {
+#ifdef ISMG_CLX_NOB
+                br_ = 0.25;
+#else
                 br_ = __ldg(brow + Irc);
+#endif
             }
             const Nbr vr = gather(rowo + Irc, pitch, true, kFive);
             const double rres = apply_lane<true, kFive, kSel>(Wr, vr, br_, fastdiv);
@@ -412,7 +430,11 @@ __device__ int cl_group(const ClGeom& T, const Band& B, const View& cbg, ClShare
         const long long c1 = clock64();
         tr_int += c1 - c0;
 #endif
+#ifdef ISMG_CLX_NOSYNC
+        if (tau == tau_end) step_sync(B);
+#else
         if (S == 1 || tau % S == S - 1 || tau == tau_end) step_sync(B);  // S: template constant
+#endif
         else __syncwarp();
 #ifdef ISMG_CL_TRACE
         tr_bar += clock64() - c1;
@@ -701,20 +723,24 @@ void set_attrs(size_t smem) {
 
 }  // namespace
 
-// Host plan: stencil classes (interior constant + tabulated boundary ring),
-// cluster size and band height so the band fits shared memory.
-bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem, int band_min) {
+// Stencil classes of a non-periodic coarse operator: the interior rows' stencil
+// (bit for bit one class), the boundary ring tabulated by class. Table layout
+// (spec): classes 0..ncls-1 (ring), class ncls (interior), 10 doubles each (w0..w8,
+// RN(1 / w0)), then the ring's class ids as ints (row 0 by I, row ncy-1 by ncx + I,
+// column 0 by 2 ncx + J, column ncx-1 by 2 ncx + ncy + J). kind bit 0: five-point;
+// bit 1: some zero weight faces a cell inside the grid (the engines then skip it).
+bool stencil_classes(const CoarseOpH& op, StencilClasses& S) {
     if (op.px || op.py || op.ncx < 3 || op.ncy < 3) return false;
-    T.ncx = op.ncx, T.ncy = op.ncy, T.five = op.five_point;
-    T.ring = 2 * op.ncx + 2 * op.ncy;
-    for (int sl = 0; sl < 9; ++sl) T.stdw[sl] = op.at(sl, 1, 1);
+    S.five = op.five_point;
+    S.ring = 2 * op.ncx + 2 * op.ncy;
+    for (int sl = 0; sl < 9; ++sl) S.stdw[sl] = op.at(sl, 1, 1);
     for (int J = 1; J < op.ncy - 1; ++J)
         for (int I = 1; I < op.ncx - 1; ++I)
             for (int sl = 0; sl < 9; ++sl)
-                if (!same_bits(op.at(sl, I, J), T.stdw[sl])) return false;
-    if (T.stdw[0] == 0.0) return false;
+                if (!same_bits(op.at(sl, I, J), S.stdw[sl])) return false;
+    if (S.stdw[0] == 0.0) return false;
     std::vector<std::array<double, 9>> cls;
-    std::vector<int> ring_cls(size_t(T.ring), 0);
+    std::vector<int> ring_cls(size_t(S.ring), 0);
     auto classify = [&](int r, int I, int J) {
         std::array<double, 9> w;
         for (int sl = 0; sl < 9; ++sl) w[sl] = op.at(sl, I, J);
@@ -729,30 +755,29 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
     };
     for (int I = 0; I < op.ncx; ++I) classify(I, I, 0), classify(op.ncx + I, I, op.ncy - 1);
     for (int J = 0; J < op.ncy; ++J) classify(2 * op.ncx + J, 0, J), classify(2 * op.ncx + op.ncy + J, op.ncx - 1, J);
-    T.ncls = int(cls.size());
-    if (T.ncls > 1024) return false;
-    T.fastdiv = 1;  // div_cr (kernels.cuh): correctly rounded for every divisor; the sample below is a sanity check
-    T.stdy = 1.0 / T.stdw[0];
+    S.ncls = int(cls.size());
+    if (S.ncls > 1024) return false;
+    S.fastdiv = 1;  // div_cr (kernels.cuh): correctly rounded for every divisor; the sample below is a sanity check
     uint64_t st = 0x9E3779B97F4A7C15ull;
     for (size_t c = 0; c <= cls.size(); ++c) {
-        const double b = c < cls.size() ? cls[c][0] : T.stdw[0];
+        const double b = c < cls.size() ? cls[c][0] : S.stdw[0];
         if (b == 0.0) return false;  // singular ring row: the op-level path raises
         const double y = 1.0 / b;
-        for (int k = 0; k < 20000 && T.fastdiv; ++k) {
+        for (int k = 0; k < 20000 && S.fastdiv; ++k) {
             st ^= st << 13, st ^= st >> 7, st ^= st << 17;
             const double a = std::ldexp(double(st >> 11) * 0x1.0p-53 + 0.5, int((st >> 3) % 120) - 60) *
                              ((st & 1) ? -1.0 : 1.0);
             const double q = a * y, r = std::fma(-q, b, a), mk = std::fma(r, y, q);
-            if (!same_bits(mk, a / b)) T.fastdiv = 0;
+            if (!same_bits(mk, a / b)) S.fastdiv = 0;
         }
     }
     // zero weights facing only ghosts (+0.0) need no skip (see term()); corners
     // of a five-point operator are never read
     static const int dx[9] = {0, 1, -1, 0, 0, 1, -1, 1, -1}, dy[9] = {0, 0, 0, 1, -1, 1, 1, -1, -1};
-    const int nsl = T.five ? 5 : 9;
+    const int nsl = S.five ? 5 : 9;
     bool zghost = true;
-    for (int sl = 1; sl < nsl; ++sl) zghost = zghost && T.stdw[sl] != 0.0;
-    for (int r = 0; r < T.ring && zghost; ++r) {
+    for (int sl = 1; sl < nsl; ++sl) zghost = zghost && S.stdw[sl] != 0.0;
+    for (int r = 0; r < S.ring && zghost; ++r) {
         int I, J;
         if (r < op.ncx) I = r, J = 0;
         else if (r < 2 * op.ncx) I = r - op.ncx, J = op.ncy - 1;
@@ -764,16 +789,28 @@ bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, s
             if (cls[size_t(ring_cls[size_t(r)])][size_t(sl)] == 0.0 && !ghost) zghost = false;
         }
     }
-    T.kind = (T.five ? 1 : 0) | (zghost ? 0 : 2);
-    T.role = 0;
-    // table: classes 0..ncls-1 (ring), class ncls (interior), then the ring's class ids
-    spec.assign(size_t(10) * (T.ncls + 1) + size_t(T.ring + 1) / 2, 0.0);
-    for (int c = 0; c <= T.ncls; ++c) {
-        const double* w = c < T.ncls ? cls[size_t(c)].data() : T.stdw;
-        for (int sl = 0; sl < 9; ++sl) spec[size_t(10) * c + sl] = w[sl];
-        spec[size_t(10) * c + 9] = 1.0 / w[0];
+    S.kind = (S.five ? 1 : 0) | (zghost ? 0 : 2);
+    S.spec.assign(size_t(10) * (S.ncls + 1) + size_t(S.ring + 1) / 2, 0.0);
+    for (int c = 0; c <= S.ncls; ++c) {
+        const double* w = c < S.ncls ? cls[size_t(c)].data() : S.stdw;
+        for (int sl = 0; sl < 9; ++sl) S.spec[size_t(10) * c + sl] = w[sl];
+        S.spec[size_t(10) * c + 9] = 1.0 / w[0];
     }
-    std::memcpy(spec.data() + size_t(10) * (T.ncls + 1), ring_cls.data(), sizeof(int) * ring_cls.size());
+    std::memcpy(S.spec.data() + size_t(10) * (S.ncls + 1), ring_cls.data(), sizeof(int) * ring_cls.size());
+    return true;
+}
+
+// Host plan: stencil classes (interior constant + tabulated boundary ring),
+// cluster size and band height so the band fits shared memory.
+bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem, int band_min) {
+    StencilClasses S;
+    if (!stencil_classes(op, S)) return false;
+    T.ncx = op.ncx, T.ncy = op.ncy, T.five = S.five;
+    T.ring = S.ring, T.ncls = S.ncls, T.fastdiv = S.fastdiv, T.kind = S.kind;
+    for (int sl = 0; sl < 9; ++sl) T.stdw[sl] = S.stdw[sl];
+    T.stdy = 1.0 / T.stdw[0];
+    T.role = 0;
+    spec = S.spec;
     // pitches = 3 (mod 16) doubles (conflict-free wavefront lanes), >= ncx + 2
     T.pitch = (op.ncx + 2) + ((3 - (op.ncx + 2) % 16) + 16) % 16;
     T.bpitch = op.ncx + ((3 - op.ncx % 16) + 16) % 16;

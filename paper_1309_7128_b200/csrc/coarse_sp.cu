@@ -1,0 +1,614 @@
+// coarse_sp.cu — the coarse visit (cycles.hpp:120-137; coarsening.hpp:531-567)
+// as a pipeline of whole sweeps over the SMs.
+//
+// gs_sweep_lex is lexicographic Gauss-Seidel: cell (I,J) of sweep g needs the
+// sweep-g values of W, SW, S, SE and the sweep-(g-1) values of E, NW, N, NE.
+// Within one sweep the cells on a diagonal I + 2J are independent, so a sweep
+// is a wavefront of ncx + 2 ncy steps; between sweeps the only dependency is
+// "sweep g reads what sweep g-1 wrote, a few columns ahead". This engine gives
+// every sweep its own CTA (one per SM, cooperative launch):
+//
+//  * inside the CTA, lane l of compute warp b owns row J = 32 b + l; block b
+//    runs kStride = 64 + kD steps behind block b-1 (the skew kD lets the warps
+//    meet at a named barrier only every kS steps). The wavefront's critical
+//    path never leaves the SM: in-warp neighbours through a shared-memory ring
+//    of the sweep's new values, block edges mirrored into the neighbour warp's
+//    ring;
+//  * the sweep-(g-1) values and the rhs arrive by cp.async, kK steps ahead,
+//    from L2 buffers in a diagonal layout (a warp's 32 lanes read 256
+//    contiguous bytes per step); the sweep's own values go out the same way;
+//  * CTA g runs ~30 steps behind CTA g-1: a comm warp per CTA publishes the
+//    CTA's progress (release, gpu scope) and polls its predecessor's, so the
+//    SM-to-SM latency (~1 us) sits in that lag, not in the wavefront;
+//  * the residual of sweep g (coarse_residual, for the stop test after every
+//    sweep) is formed kR steps behind the update from the same ring; the CTA
+//    folds the sweep's max|r| and Σx (anchor) when the sweep ends.
+//
+// Sweeps are taken in order by the CTAs (CTA c: sweeps c, c + P, ...), each
+// writing its own buffer (ring of B = P + 2), so no checkpoint and no replay:
+// the first sweep whose residual passes tol_coarse is the answer; later sweeps
+// in flight abort. A visit of G sweeps costs one wavefront plus G-1 lags; a
+// long visit runs P sweeps at once. Results are the reference's bit for bit
+// (same per-cell operation order; division correctly rounded, kernels.cuh).
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "fused_impl.cuh"
+
+namespace ismgb {
+namespace fz {
+
+namespace {
+
+constexpr int kS = 4;                  // steps between named barriers of the compute warps
+constexpr int kD = kS - 1;             // skew between consecutive 32-row blocks (steps)
+constexpr int kR = 3 + kD + kS;        // residual lag (steps): row 32's mirror value is >= kS steps old
+constexpr int kK = 5;                  // cp.async prefetch distance (steps)
+constexpr int kQ = 24;                 // new-value ring slots (3 segments of 8)
+constexpr int kQE = 8, kQB = 16;       // old-value / rhs ring slots
+constexpr int kRows = 34;              // ring rows: block rows -1 .. 32
+constexpr int kMaxW = 16;              // compute warps (32-row blocks)
+constexpr int kStride = 64 + kD;       // CTA steps between consecutive blocks
+constexpr int kDLo = -4;               // first diagonal of a block's loop (ghost columns written as 0)
+constexpr int kDHiPad = 63;            // last update diagonal: ncx + kDHiPad
+constexpr int kDOff = 72;              // layouts: diagonal d of block b at [b][d + kDOff][lane]
+constexpr int kDSpanPad = 168;         // diagonals per block: ncx + kDSpanPad
+constexpr int kSpThreads = 32 * (kMaxW + 1);
+constexpr int kInf = INT_MAX;
+
+static_assert(kK + kR + 1 <= kQB, "rhs ring: slots of the residual's rhs live until the update overwrites them");
+static_assert(kK + 1 <= kQE, "old-value ring");
+static_assert(kD + kR + 2 * kS <= kQ, "new-value ring: live span (mirror writes ahead, residual reads behind)");
+static_assert(kK - 2 >= 1, "prefetch must run ahead of the NE read (t + 2)");
+
+__device__ unsigned g_sp_stuck = 0u;  // watchdog: a wait ran past 2 s
+
+}  // namespace
+
+struct SpK {
+    int ncx, ncy, nb;        // coarse grid, 32-row blocks (= compute warps)
+    int P, B;                // CTAs (sweeps in flight), buffers
+    int dspan;               // diagonals per block in the layouts
+    int64_t bstride, bufsz;  // doubles per block / per buffer
+    int ncls, ring, spec_words;
+    int singular;
+    int tend;                // last CTA step of a sweep
+};
+
+struct SpD {
+    double* bufs;                // [B][nb][dspan][32] sweep outputs (diagonal layout)
+    double* zero;                // one all-zero buffer: sweep -1 (ce = 0) and missing blocks
+    double* bd;                  // rhs, diagonal layout
+    const double* spec;          // class table (stencil_classes)
+    unsigned long long* prog;    // [P] progress: (sweep << 32) | steps done (0xffffffff: sweep finished)
+    unsigned* finw;              // [B] sweep g done: finw[g % B] = g + 1
+    double* resw;                // [B] residual max of sweep g
+    double* sumw;                // [B] Σ x of sweep g (anchor)
+    int* st;                     // [0] first converged sweep (INT_MAX none), [1] sweeps finished
+    unsigned* bar;               // grid barrier: [0] arrivals, [1] generation
+};
+
+namespace {
+
+extern __shared__ __align__(16) double sp_dyn[];
+
+__device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bar_compute(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+__device__ __forceinline__ int ld_acq_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(su32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(su32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_vol_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acq_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_rlx_gpu(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_rel_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ bool timed_out(long long t0) {
+    if (gtimer() - t0 > 2000000000ll) {
+        atomicExch(&g_sp_stuck, 1u);
+        return true;
+    }
+    return false;
+}
+
+__device__ void sp_grid_sync(unsigned* bar, unsigned n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vb = bar;
+        const unsigned gen = vb[1];
+        __threadfence();
+        if (atomicAdd(bar, 1u) == n - 1) {
+            vb[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            const long long t0 = gtimer();
+            while (vb[1] == gen) {
+                __nanosleep(32);
+                if (timed_out(t0)) break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct SpShared {
+    int avail;      // steps of sweep g-1 available (from the comm warp)
+    int abort_;     // sweep g > first converged sweep: stop
+    int done_t;     // steps of this sweep done (for the comm warp to publish)
+    int end;        // compute warps finished the sweep
+    int aborted;
+    int go;
+    int dec[2];     // abort decision per barrier parity
+    double wmax[kMaxW], wsum[kMaxW];
+};
+
+// correctly rounded num / w with y = RN(1 / w) (kernels.cuh div_cr), every lane active
+__device__ __forceinline__ double div_full(double num, double w, double y) {
+#ifdef ISMG_SPX_NODIV
+    return num * y;
+#endif
+    const unsigned e = unsigned(__double2hiint(num)) & 0x7ff00000u;
+    const bool bad = e - (123u << 20) > (1900u << 20);
+    const double q0 = __dmul_rn(num, y);
+    const double e0 = __fma_rn(-q0, w, num);
+    const double q1 = __fma_rn(e0, y, q0);
+    const double e1 = __fma_rn(-q1, w, num);
+    double q = __fma_rn(e1, y, q1);
+    if (__any_sync(kFull, bad)) q = div_ieee_lanes(num, w, q, bad);
+    return q;
+}
+
+// One sweep of one compute warp (32-row block b) over CTA steps -8 .. tend.
+// Lane l: row J = 32 b + l, update column I = d - 2 l, residual column I - kR,
+// d = t + kDLo - kStride b. Per step: prefetch (cp.async) for step t + kK, the
+// update (weights of the cell's class from the table: west column, row body,
+// east column), the residual kR columns behind, a named barrier every kS steps.
+__device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& sh, double* ringN, double* ringE,
+                                         double* ringB, double* ringX, const double* tbl, const int* ring_cls,
+                                         const double* __restrict__ xo, double* __restrict__ xn, int g) {
+    const int b = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nthr = 32 * T.nb;
+    const int ncx = T.ncx, ncy = T.ncy;
+    const int J = 32 * b + lane;
+    const bool rowok = J < ncy;
+    const int dhi = ncx + kDHiPad;
+    // classes of this lane's row: column 0, columns 1 .. ncx-2 (one class, checked by the plan), column ncx-1
+    int wcls = T.ncls, bcls = T.ncls, ecls = T.ncls;
+    if (rowok) {
+        if (J == 0 || J == ncy - 1) {
+            const int rb = J == 0 ? 0 : ncx;
+            wcls = ring_cls[rb], bcls = ring_cls[rb + 1], ecls = ring_cls[rb + ncx - 1];
+        } else {
+            wcls = ring_cls[2 * ncx + J], ecls = ring_cls[2 * ncx + ncy + J];
+        }
+    }
+    // rings of this warp (new values: [kQ][kRows]; the neighbour blocks' rings sit kQ kRows doubles away)
+    double* rN = ringN + size_t(b) * kQ * kRows;
+    double* rE = ringE + size_t(b) * kQE * 32 + lane;
+    double* rB = ringB + size_t(b) * kQB * 32 + lane;
+    double* rX = ringX + size_t(b) * kQE;
+    const uint32_t sE = su32(rE), sB = su32(rB), sX = su32(rX);
+    const bool has_n = b + 1 < T.nb, has_p = b > 0;
+    const double* xo_b = xo + size_t(b) * T.bstride + lane;
+    const double* xo_n = (has_n ? xo + size_t(b + 1) * T.bstride : D.zero);  // row 32 (b+1) = next block's lane 0
+    const double* bd_b = D.bd + size_t(b) * T.bstride + lane;
+    double* xn_b = xn + size_t(b) * T.bstride + lane;
+    // update: W (own previous output), S / SW (previous SE), N / NW (previous NE)
+    double outP = 0.0, seP = 0.0, seP2 = 0.0, neP = 0.0, neP2 = 0.0;
+    // residual window: rows r-1 (S*), r (W C E), r+1 (N*)
+    double qSW = 0.0, qS = 0.0, qSE = 0.0, qW = 0.0, qC = 0.0, qE = 0.0, qNW = 0.0, qN = 0.0, qNE = 0.0;
+    double lmax = 0.0, rsum = 0.0;
+    int avail = g == 0 ? kInf : 0;
+    int h = 0;
+    bool aborted = false;
+    const int mend = T.tend >> 3;
+    for (int m = -1; m <= mend && !aborted; ++m) {
+        // new-value ring segments (8 slots each) of steps 8(m-1).., 8m.., 8(m+1).. (= 8(m-2)..)
+        const int m3 = (m + 3) % 3;
+        const int sA = ((m3 + 2) % 3) * 8 * kRows, sBn = m3 * 8 * kRows, sC = ((m3 + 1) % 3) * 8 * kRows;
+        const int b0 = (m & 1) * 8 * 32, b1 = ((m + 1) & 1) * 8 * 32;  // rhs ring segments by parity
+        const int d0 = 8 * m + kDLo - kStride * b;                       // diagonal of step j = 0
+        const size_t o0 = size_t(d0 + kDOff) * 32;                        // layout offset of d0 (d0 + kDOff >= 0)
+        const double* pE = xo_b + o0 + size_t(kK + 1) * 32;              // E of step j + kK: diagonal d + kK + 1
+        const double* pB = bd_b + o0 + size_t(kK) * 32;
+        const double* pX = xo_n + o0 + size_t(kK) * 32 - 61 * 32;        // lane 31: row 32, column I + 1
+        double* pO = xn_b + o0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int t = 8 * m + j;
+            auto nslot = [&](int q) {  // ring offset of CTA step 8m + q (q folds to a constant)
+                const int seg = q >> 3;
+                return (seg == 0 ? sBn : (seg == -1 ? sA : sC)) + (q & 7) * kRows;
+            };
+            auto bslot = [&](int q) { return (((q >> 3) & 1) ? b1 : b0) + (q & 7) * 32; };
+            if ((j & 3) == 0 && avail < t + 3 + kK + kD + 4) {  // sweep g-1 far enough for the next kS steps
+                const int need = t + 3 + kK + kD + 4;
+                if (lane == 0) {
+                    const long long tw = gtimer();
+                    int a;
+                    while ((a = ld_acq_cta(&sh.avail)) < need) {
+                        if (ld_vol_s(&sh.abort_) || timed_out(tw)) break;
+                    }
+                    avail = a;
+                }
+                avail = __shfl_sync(kFull, avail, 0);
+                __syncwarp();
+            }
+            const int d = d0 + j;
+#ifndef ISMG_SPX_NOCP
+            if (d + kK >= kDLo && d + kK <= dhi + kR) {  // prefetch for step t + kK
+                cp8(sE + 8u * uint32_t(((j + kK) & 7) * 32), pE + 32 * j);
+                cp8(sB + 8u * uint32_t(bslot(j + kK)), pB + 32 * j);
+                if (lane == 31) cp8(sX + 8u * uint32_t((j + kK) & 7), pX + 32 * j);
+            }
+#endif
+            cp_commit();
+            cp_wait<kK - 2>();
+            __syncwarp();
+            if (d >= kDLo && d <= dhi + kR) {
+                // ---- update of column I (sweep g) ----
+                const int I = d - 2 * lane;
+                const bool act_u = rowok && unsigned(I) < unsigned(ncx) && d <= dhi;
+                const double E = rE[(j & 7) * 32];
+                const double NE = lane < 31 ? rE[((j + 2) & 7) * 32 + 1] : rX[j & 7];
+                const double SE = rN[nslot(j - 1) + lane];
+                const double bu = rB[bslot(j)];
+                const double2* wu = reinterpret_cast<const double2*>(
+                    tbl + 10 * (I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls)));
+                const double2 u01 = wu[0], u23 = wu[1], u45 = wu[2], u67 = wu[3], u89 = wu[4];
+                double acc = 0.0;
+                acc += u01.y * E;
+                acc += u23.x * outP;
+                acc += u23.y * neP;
+                acc += u45.x * seP;
+                acc += u45.y * NE;
+                acc += u67.x * neP2;
+                acc += u67.y * SE;
+                acc += u89.x * seP2;
+                const double num = act_u ? bu - acc : 1.0;
+                const double q = div_full(num, u01.x, u89.y);
+                const double out = act_u ? q : 0.0;
+                rN[nslot(j) + lane + 1] = out;
+                if (lane == 31 && has_n) rN[kQ * kRows + nslot(j + kD)] = out;      // row -1 of the next block
+                if (lane == 0 && has_p) rN[nslot(j - kD) + 33 - kQ * kRows] = out;  // row 32 of the previous block
+#ifndef ISMG_SPX_NOSTG
+                if (d <= dhi) pO[32 * j] = out;
+#endif
+                if (act_u) rsum += out;
+                seP2 = seP, seP = SE, neP2 = neP, neP = NE, outP = out;
+#ifndef ISMG_SPX_NORES
+                // ---- residual of column I - kR (sweep g values on all nine points) ----
+                const int Ir = I - kR;
+                const bool act_r = rowok && unsigned(Ir) < unsigned(ncx);
+                qSW = qS, qS = qSE, qSE = rN[nslot(j - kR - 1) + lane];
+                qW = qC, qC = qE, qE = rN[nslot(j - kR + 1) + lane + 1];
+                qNW = qN, qN = qNE, qNE = rN[nslot(j - kR + 3) + lane + 2];
+                const double br = rB[bslot(j - kR)];
+                const double2* wr = reinterpret_cast<const double2*>(
+                    tbl + 10 * (Ir == 0 ? wcls : (Ir == ncx - 1 ? ecls : bcls)));
+                const double2 r01 = wr[0], r23 = wr[1], r45 = wr[2], r67 = wr[3], r89 = wr[4];
+                double a = r01.x * qC;
+                a += r01.y * qE;
+                a += r23.x * qW;
+                a += r23.y * qN;
+                a += r45.x * qS;
+                a += r45.y * qNE;
+                a += r67.x * qNW;
+                a += r67.y * qSE;
+                a += r89.x * qSW;
+                double mm = act_r ? fabs(br - a) : 0.0;
+                mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
+                lmax = fmax(lmax, mm);
+#endif
+            }
+#ifdef ISMG_SPX_NOBAR
+            if (false) {
+#else
+            if ((j & 3) == 3) {
+#endif  // named barrier of the compute warps every kS steps
+                if (b == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
+                bar_compute(nthr);
+                if (b == 0 && lane == 0) st_rel_cta(&sh.done_t, max(0, t + 1));
+                aborted = ld_vol_s(&sh.dec[h & 1]) != 0;
+                ++h;
+                if (aborted) break;
+            }
+        }
+    }
+    cp_wait<0>();
+    // fold: max|r| (order-free), Σx in a fixed order (lanes by tree, blocks in order)
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(kFull, lmax, o));
+    rsum = warp_sum_down(rsum);
+    if (lane == 0) sh.wmax[b] = lmax, sh.wsum[b] = rsum;
+    bar_compute(nthr);
+    if (b == 0 && lane == 0) {
+        sh.aborted = aborted ? 1 : 0;
+        *reinterpret_cast<volatile int*>(&sh.end) = 1;
+    }
+}
+
+// The comm warp of a sweep: predecessor's progress in, this CTA's out, stop flag.
+__device__ __forceinline__ void sp_comm(const SpD& D, SpShared& sh, int g, int P) {
+    if ((threadIdx.x & 31) == 0) {
+        const unsigned long long prev_hi = (unsigned long long)(unsigned(g - 1)) << 32;
+        const unsigned long long* pp = D.prog + (g > 0 ? (g - 1) % P : 0);
+        unsigned long long* me = D.prog + blockIdx.x;
+        int avail = g == 0 ? kInf : 0, last = -1;
+        const long long t0 = gtimer();
+        while (!ld_vol_s(&sh.end)) {
+            if (avail < kInf) {
+                const unsigned long long v = ld_acq_gpu(pp);
+                if (v >= prev_hi) {
+                    const unsigned lo = unsigned(v & 0xffffffffull);
+                    const int a = ((v >> 32) > (unsigned long long)(g - 1) || lo == 0xffffffffu) ? kInf : int(lo);
+                    if (a > avail) avail = a, st_rel_cta(&sh.avail, a);
+                }
+            }
+            const int dt = ld_acq_cta(&sh.done_t);
+            if (dt != last) {
+                last = dt;
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(me),
+                             "l"(((unsigned long long)(unsigned)g << 32) | unsigned(dt))
+                             : "memory");
+            }
+            if (ld_rlx_gpu(D.st) < g) *reinterpret_cast<volatile int*>(&sh.abort_) = 1;
+            if (timed_out(t0)) *reinterpret_cast<volatile int*>(&sh.abort_) = 1;
+        }
+    }
+    __syncwarp();
+}
+
+// thread 0: may sweep g start? 1 go, 0 stop (past the first converged sweep or the budget)
+__device__ int sp_start(const SpK& T, const SpD& D, int g, long long budget, int a0) {
+    const long long t0 = gtimer();
+    for (;;) {
+        if (g >= budget || g > ld_rlx_gpu(D.st)) return 0;
+        bool ok = g < a0 + 2 * ld_rlx_gpu(D.st + 1);  // at most a0 + 2 x (sweeps finished) in flight
+        if (ok && g >= T.B)  // buffer g % B: sweep g-B decided, sweep g-B+1 done reading it
+            ok = ld_acq_gpu(D.finw + g % T.B) == unsigned(g - T.B + 1) &&
+                 ld_acq_gpu(D.finw + (g + 1) % T.B) == unsigned(g - T.B + 2);
+        if (ok) return g > ld_rlx_gpu(D.st) ? 0 : 1;
+        __nanosleep(64);
+        if (timed_out(t0)) return 0;
+    }
+}
+
+__global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK T, SpD D) {
+    Ctl* st = P.ctl;
+    if (st->phase != kCoarse) return;
+    const long long t_start = gtimer();
+    __shared__ SpShared sh;
+    const int NW = T.nb;
+    const int warp = threadIdx.x >> 5;
+    // shared memory: new-value rings [NW][kQ][kRows] | old [NW][kQE][32] | rhs [NW][kQB][32] | X [NW][kQE] | table
+    double* ringN = sp_dyn;
+    double* ringE = ringN + size_t(NW) * kQ * kRows;
+    double* ringB = ringE + size_t(NW) * kQE * 32;
+    double* ringX = ringB + size_t(NW) * kQB * 32;
+    double* tbl = ringX + size_t(NW) * kQE;
+    const int* ring_cls = reinterpret_cast<const int*>(tbl + 10 * (T.ncls + 1));
+    const double rc0 = st->rc;  // max|cb|, formed by the fine pass that restricted
+    const long long budget = P.max_total - st->total;
+    const int pred = st->pred;
+    const bool run = rc0 > P.tol_coarse && budget > 0;
+    const unsigned nthreads = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0) {  // per-visit state (nobody else touches it before the barrier)
+        for (int k = threadIdx.x; k < T.P; k += blockDim.x) D.prog[k] = 0ull;
+        for (int k = threadIdx.x; k < T.B; k += blockDim.x) D.finw[k] = 0u;
+        if (threadIdx.x == 0) D.st[0] = kInf, D.st[1] = 0;
+    }
+    for (int k = threadIdx.x; k < T.spec_words; k += blockDim.x) tbl[k] = D.spec[k];
+    for (int k = threadIdx.x; k < NW * kQ * kRows; k += blockDim.x) ringN[k] = 0.0;  // rows -1 / 32 at the grid edge stay 0
+    if (run) {  // the rhs into the diagonal layout: bd[b][d][l] = cb(d - 2 l, 32 b + l), 0 off the grid
+        const int64_t n = int64_t(T.nb) * T.bstride;
+        for (int64_t k = gtid; k < n; k += nthreads) {
+            const int b = int(k / T.bstride);
+            const int rem = int(k - int64_t(b) * T.bstride);
+            const int l = rem & 31, d = (rem >> 5) - kDOff;
+            const int I = d - 2 * l, J = 32 * b + l;
+            D.bd[k] = (J < T.ncy && unsigned(I) < unsigned(T.ncx)) ? P.cb.at(I, J) : 0.0;
+        }
+    }
+    sp_grid_sync(D.bar, gridDim.x);  // everyone has read Ctl; rhs and state ready
+    const int a0 = 2 * max(1, pred) + 2;
+    long long steps = 0;
+    if (run) {
+        for (int g = blockIdx.x;; g += gridDim.x) {
+            if (threadIdx.x == 0) {
+                sh.go = sp_start(T, D, g, budget, a0);
+                sh.avail = g == 0 ? kInf : 0, sh.abort_ = 0, sh.done_t = 0, sh.end = 0, sh.aborted = 0;
+                sh.dec[0] = sh.dec[1] = 0;
+            }
+            __syncthreads();
+            if (!sh.go) break;
+            const double* xo = g == 0 ? D.zero : D.bufs + size_t((g - 1) % T.B) * T.bufsz;
+            double* xn = D.bufs + size_t(g % T.B) * T.bufsz;
+            if (warp == NW) sp_comm(D, sh, g, T.P);
+            else sp_sweep(T, D, sh, ringN, ringE, ringB, ringX, tbl, ring_cls, xo, xn, g);
+            __syncthreads();
+            if (threadIdx.x == 0 && !sh.aborted) {
+                double res = 0.0, sum = 0.0;
+                for (int w = 0; w < NW; ++w) res = fmax(res, sh.wmax[w]);
+                for (int w = 0; w < NW; ++w) sum += sh.wsum[w];
+                D.resw[g % T.B] = res, D.sumw[g % T.B] = sum;
+                if (!(res > P.tol_coarse)) atomicMin(D.st, g);
+                __threadfence();
+                st_rel_gpu(D.finw + g % T.B, unsigned(g + 1));
+                atomicAdd(D.st + 1, 1);
+                st_rel_gpu(D.prog + blockIdx.x, ((unsigned long long)(unsigned)g << 32) | 0xffffffffull);
+            }
+            __syncthreads();
+        }
+    }
+    sp_grid_sync(D.bar, gridDim.x);
+    int done = 0;
+    double rc = rc0, sum = 0.0;
+    const double* xk = nullptr;
+    if (run) {
+        const int first = *reinterpret_cast<volatile int*>(D.st);
+        const int k = first < budget ? first : int(budget - 1);
+        done = k + 1;
+        rc = *reinterpret_cast<volatile double*>(D.resw + k % T.B);
+        sum = *reinterpret_cast<volatile double*>(D.sumw + k % T.B);
+        xk = D.bufs + size_t(k % T.B) * T.bufsz;
+        steps = T.tend + 1;
+    }
+    // ce = the answer (anchored once when singular), natural layout
+    const bool anchor = P.singular && done > 0;
+    const double c = anchor ? -(sum / double(int64_t(T.ncx) * T.ncy)) : 0.0;
+    const int64_t ncell = int64_t(T.ncx) * T.ncy;
+    for (int64_t k = gtid; k < ncell; k += nthreads) {
+        const int J = int(k / T.ncx), I = int(k - int64_t(J) * T.ncx);
+        double v = 0.0;
+        if (xk) {
+            const int l = J & 31, b = J >> 5;
+            v = xk[size_t(b) * T.bstride + size_t(I + 2 * l + kDOff) * 32 + l];
+            if (anchor) v += c;
+        }
+        P.ce.at(I, J) = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->coarse_launches += 1;
+        st->coarse_ns += gtimer() - t_start;
+        st->coarse_steps += steps;
+        st->coarse_group_ns += gtimer() - t_start;
+        if (done > 0) st->pred = done;
+        st->total += done;
+        st->coarse += done;
+        st->rc = rc;
+        if (st->nvisits > 0 && st->nvisits <= P.visit_cap) P.visit_log[2 * (st->nvisits - 1)] = done;
+        if (*(volatile unsigned*)&g_sp_stuck) st->mp_error = 2;
+        if (rc > P.tol_coarse || st->mp_error) {  // cycles.hpp:134-137
+            st->phase = kDone, st->converged = 0;
+        } else if (done > 0) {
+            st->phase = kProlong;
+        } else {
+            st->prev = st->r;
+            st->phase = kFine;
+        }
+        publish_phase(P, st->phase);
+    }
+}
+
+}  // namespace
+
+struct SpEngine {
+    SpK T{};
+    SpD D{};
+    void* mem = nullptr;
+    size_t smem = 0;
+};
+
+// Host plan: a non-periodic 9-point operator whose zero weights face only ghosts
+// (StencilClasses kind 0), at most 16 blocks of 32 rows, every CTA resident.
+SpEngine* sp_try_create(const CoarseOpH& op, int device) {
+    if (const char* e = getenv("ISMG_COARSE_SP"))
+        if (e[0] == '0') return nullptr;
+    StencilClasses S;
+    if (!stencil_classes(op, S) || S.kind != 0 || !S.fastdiv) return nullptr;
+    const int nb = (op.ncy + 31) / 32;
+    if (nb > kMaxW) return nullptr;
+    {  // the first / last row: one class on columns 1 .. ncx-2 (the kernel's row body)
+        const int* rc = reinterpret_cast<const int*>(S.spec.data() + size_t(10) * (S.ncls + 1));
+        for (int I = 2; I < op.ncx - 1; ++I)
+            if (rc[I] != rc[1] || rc[op.ncx + I] != rc[op.ncx + 1]) return nullptr;
+    }
+    SpK T{};
+    T.ncx = op.ncx, T.ncy = op.ncy, T.nb = nb;
+    T.dspan = op.ncx + kDSpanPad;
+    T.bstride = int64_t(T.dspan) * 32;
+    T.bufsz = T.bstride * nb;
+    T.ncls = S.ncls, T.ring = S.ring;
+    T.spec_words = int(S.spec.size());
+    T.singular = op.singular ? 1 : 0;
+    T.tend = (op.ncx + kDHiPad + kR - kDLo) + kStride * (nb - 1);
+    const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * 32 + kQB * 32 + kQE) + S.spec.size());
+    ISMG_CUDA(cudaFuncSetAttribute(coarse_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0, sms = 0;
+    ISMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_sp_kernel, 32 * (nb + 1), smem));
+    ISMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (per_sm < 1) return nullptr;
+    int P = sms;
+    if (const char* e = getenv("ISMG_SP_CTAS")) P = std::max(1, std::min(sms, atoi(e)));  // tuning hook
+    T.P = P, T.B = P + 2;
+    auto* e = new SpEngine();
+    e->T = T;
+    e->smem = smem;
+    const size_t bufb = sizeof(double) * size_t(T.bufsz);
+    const size_t bytes = bufb * size_t(T.B + 2) + sizeof(double) * S.spec.size() + sizeof(unsigned long long) * P +
+                         sizeof(unsigned) * T.B + 2 * sizeof(double) * T.B + 64 + 1024;
+    ISMG_CUDA(cudaMalloc(&e->mem, bytes));
+    ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
+    char* p = static_cast<char*>(e->mem);
+    e->D.bufs = reinterpret_cast<double*>(p), p += bufb * T.B;
+    e->D.zero = reinterpret_cast<double*>(p), p += bufb;
+    e->D.bd = reinterpret_cast<double*>(p), p += bufb;
+    double* spec = reinterpret_cast<double*>(p);
+    ISMG_CUDA(cudaMemcpy(spec, S.spec.data(), sizeof(double) * S.spec.size(), cudaMemcpyHostToDevice));
+    e->D.spec = spec, p += sizeof(double) * S.spec.size();
+    e->D.resw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;
+    e->D.sumw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;
+    e->D.prog = reinterpret_cast<unsigned long long*>(p), p += sizeof(unsigned long long) * P;
+    e->D.finw = reinterpret_cast<unsigned*>(p), p += sizeof(unsigned) * T.B;
+    p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 63) & ~uintptr_t(63));
+    e->D.st = reinterpret_cast<int*>(p), p += 64;
+    e->D.bar = reinterpret_cast<unsigned*>(p);
+    return e;
+}
+
+void sp_destroy(SpEngine* e) {
+    if (!e) return;
+    cudaFree(e->mem);
+    delete e;
+}
+
+void launch_coarse_sp(const Params& P, const SpEngine& e, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(e.T.P));
+    cfg.blockDim = dim3(unsigned(32 * (e.T.nb + 1)));
+    cfg.dynamicSmemBytes = e.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ISMG_CUDA(cudaLaunchKernelEx(&cfg, coarse_sp_kernel, P, e.T, e.D));
+}
+
+}  // namespace fz
+}  // namespace ismgb

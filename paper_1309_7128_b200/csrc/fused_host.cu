@@ -30,8 +30,9 @@ struct FusedEngine {
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
     int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands,
-                             // 4 register wavefront over many SMs
+                             // 4 register wavefront over many SMs, 5 sweep pipeline over the SMs
     RwEngine* rw = nullptr;
+    SpEngine* sp = nullptr;
     TmGeom tm{};
     ClGeom cl{};
     // hybrid coarse visits: a one-SM kernel (cl1, role 1) runs groups of <= 4
@@ -75,7 +76,9 @@ static int launch_fine(const FusedEngine& e, cudaStream_t st, bool sweep_only = 
 
 // the coarse-visit kernel(s) of this engine with parameters P
 static void launch_coarse(const FusedEngine& e, const Params& P, cudaStream_t st) {
-    if (e.coarse_kind == 4) {
+    if (e.coarse_kind == 5) {
+        launch_coarse_sp(P, *e.sp, st);
+    } else if (e.coarse_kind == 4) {
         launch_coarse_rw(P, *e.rw, st);
     } else if (e.coarse_kind == 3) {
         if (e.cl_hybrid) launch_coarse_cl(P, e.cl1, e.tm_spec, e.coarse_backup1, e.coarse_smem1, st);
@@ -170,15 +173,21 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     return ge;
 }
 
-// The coarse-visit kernel of level h: the cluster engine where it plans (coarse
-// grids up to 16 x 32-row bands), the register wavefront beyond it (config 4's
+// The coarse-visit kernel of level h: the sweep pipeline where it plans (coarse
+// grids up to 16 blocks of 32 rows, every zero weight facing a ghost), else the
+// cluster engine (up to 16 x 32-row bands), the register wavefront (config 4's
 // 512 x 1024 level), then TMEM-resident rhs, shared-memory iterate, global
 // wavefront. P.ncx / P.ncy must be set.
 static void plan_coarse(FusedEngine& ee, const CoarseOpH& h, int device) {
     FusedEngine* e = &ee;
     Params& P = e->P;
     std::vector<double> spec;
-    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "rw" | "cl" | "tmem" | "smem" | "global"
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "sp" | "rw" | "cl" | "tmem" | "smem" | "global"
+    const bool allow_sp = !force || std::string(force) == "sp";
+    if (allow_sp && (e->sp = sp_try_create(h, device)) != nullptr) {
+        e->coarse_kind = 5;
+        return;
+    }
     const bool allow_rw = !force || std::string(force) == "rw";
     const bool allow_cl = !force || std::string(force) == "cl";
     const bool allow_tmem = !force || std::string(force) == "tmem";
@@ -423,6 +432,7 @@ void destroy_fused(FusedEngine* e) {
     cudaFree(e->tm_spec);
     cudaFree(e->coarse_backup1);
     rw_destroy(e->rw);
+    sp_destroy(e->sp);
     for (void* p : e->peer_map)
         if (p) cudaIpcCloseMemHandle(p);
     cudaFree(e->xbuf);

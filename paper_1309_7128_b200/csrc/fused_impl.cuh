@@ -359,6 +359,14 @@ struct ClGeom {
     double stdw[9];  // interior weights (slot order C, E, W, N, S, NE, NW, SE, SW)
     double stdy;     // RN(1 / stdw[0]): Markstein's reciprocal (fastdiv)
 };
+// Stencil classes of a non-periodic coarse operator (coarse_cl.cu)
+struct StencilClasses {
+    int ncls = 0, ring = 0, kind = 0, fastdiv = 0;
+    bool five = false;
+    double stdw[9] = {};      // interior weights
+    std::vector<double> spec;  // [ncls + 1][10] (w0..w8, RN(1 / w0); interior last), then ring class ids (int)
+};
+bool stencil_classes(const CoarseOpH& op, StencilClasses& S);
 bool cl_coarse_plan(const CoarseOpH& op, ClGeom& T, std::vector<double>& spec, size_t& smem, int band_min = 0);
 size_t cl_backup_doubles(const ClGeom& T);
 void launch_coarse_cl(const Params& P, const ClGeom& T, const double* spec, double* backup, size_t smem,
@@ -372,6 +380,13 @@ RwEngine* rw_try_create(const CoarseOpH& op, int device);
 void rw_destroy(RwEngine* e);
 void launch_coarse_rw(const Params& P, const RwEngine& e, cudaStream_t st);
 std::vector<double> rw_trace_take();
+
+// Sweep pipeline over the SMs (coarse_sp.cu): one CTA per sweep; nullptr when
+// the operator does not fit it.
+struct SpEngine;
+SpEngine* sp_try_create(const CoarseOpH& op, int device);
+void sp_destroy(SpEngine* e);
+void launch_coarse_sp(const Params& P, const SpEngine& e, cudaStream_t st);
 
 bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem);
 void launch_coarse_tmem(const Params& P, const TmGeom& T, const double* spec, double* backup, size_t smem,

@@ -136,7 +136,7 @@ def test_zero_rhs_and_budget(dev):
         assert not rep.converged and rep.fine_sweeps + rep.coarse_sweeps <= 3
 
 
-@pytest.mark.parametrize("kernel", ["cl", "tmem", "smem", "global"])
+@pytest.mark.parametrize("kernel", ["sp", "cl", "tmem", "smem", "global"])
 @pytest.mark.parametrize("which", ["lid96", "jet48x96"])
 def test_coarse_visit_kernels_match_oracle(dev, port, monkeypatch, kernel, which):
     """Every coarse-visit kernel of the fused path (TMEM-resident rhs,

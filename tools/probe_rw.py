@@ -12,7 +12,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 tile = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 g = setup_lid_cavity(n, 1000.0).grid
 ncx = (n + tile - 1) // tile
-for budget in (1, 2, 4, 8, 32, 128, 512, 2048):
+BUDGETS = [int(x) for x in os.environ.get("PROBE_BUDGETS", "1,2,4,8,32,128,512,2048").split(",")]
+for budget in BUDGETS:
     cfg = CycleConfig(tile=tile, tol_fine=1e-300, tol_coarse=1e-300, max_total_sweeps=budget)
     s = P.PressureSolver(g, cfg)
     cb = random_field(ncx, ncx, np.random.default_rng(1), -1e-3, 1e-3)
