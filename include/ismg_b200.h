@@ -150,7 +150,8 @@ typedef struct ismg_solve_stats {
     int64_t coarse_engine;      /* coarse-visit kernel of the fused path: 0 global
                                    wavefront, 1 shared-memory iterate, 2 TMEM rhs,
                                    3 cluster bands, 4 register wavefront,
-                                   5 sweep pipeline; -1 op-level */
+                                   5 sweep pipeline, 6 sweep pipeline with several
+                                   blocks per warp; -1 op-level */
 } ismg_solve_stats;
 
 /* ---- opaque handles ------------------------------------------------------ */

@@ -27,7 +27,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
           "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
-SOURCES = ["objects.cu", "geometry.cpp", "ops.cu", "fine_pass.cu", "fine_pass_w.cu", "coarse.cu", "coarse_tmem.cu", "coarse_cl.cu", "coarse_rw.cu", "coarse_sp.cu", "fused_host.cu",
+SOURCES = ["objects.cu", "geometry.cpp", "ops.cu", "fine_pass.cu", "fine_pass_w.cu", "coarse.cu", "coarse_tmem.cu", "coarse_cl.cu", "coarse_rw.cu", "coarse_sp.cu", "coarse_sp2.cu", "fused_host.cu",
            "solver.cu", "comm.cpp", "capi.cpp"]
 HEADERS = ["common.h", "engine.h", "kernels.cuh", "solver.h", "fused_impl.cuh"]
 

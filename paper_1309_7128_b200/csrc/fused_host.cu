@@ -30,9 +30,11 @@ struct FusedEngine {
     double* coarse_backup = nullptr;
     size_t coarse_smem = 0;  // dynamic shared memory of the coarse-visit kernel
     int coarse_kind = 0;     // 0 global wavefront, 1 shared-memory iterate, 2 + TMEM rhs, 3 cluster bands,
-                             // 4 register wavefront over many SMs, 5 sweep pipeline over the SMs
+                             // 4 register wavefront over many SMs, 5 sweep pipeline over the SMs,
+                             // 6 sweep pipeline with several blocks per warp (> 16 blocks)
     RwEngine* rw = nullptr;
     SpEngine* sp = nullptr;
+    Sp2Engine* sp2 = nullptr;
     TmGeom tm{};
     ClGeom cl{};
     // hybrid coarse visits: a one-SM kernel (cl1, role 1) runs groups of <= 4
@@ -76,7 +78,9 @@ static int launch_fine(const FusedEngine& e, cudaStream_t st, bool sweep_only = 
 
 // the coarse-visit kernel(s) of this engine with parameters P
 static void launch_coarse(const FusedEngine& e, const Params& P, cudaStream_t st) {
-    if (e.coarse_kind == 5) {
+    if (e.coarse_kind == 6) {
+        launch_coarse_sp2(P, *e.sp2, st);
+    } else if (e.coarse_kind == 5) {
         launch_coarse_sp(P, *e.sp, st);
     } else if (e.coarse_kind == 4) {
         launch_coarse_rw(P, *e.rw, st);
@@ -182,10 +186,15 @@ static void plan_coarse(FusedEngine& ee, const CoarseOpH& h, int device) {
     FusedEngine* e = &ee;
     Params& P = e->P;
     std::vector<double> spec;
-    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "sp" | "rw" | "cl" | "tmem" | "smem" | "global"
+    const char* force = getenv("ISMG_COARSE_KERNEL");  // test hook: "sp" | "sp2" | "rw" | "cl" | "tmem" | "smem" | "global"
     const bool allow_sp = !force || std::string(force) == "sp";
+    const bool allow_sp2 = !force || std::string(force) == "sp2";
     if (allow_sp && (e->sp = sp_try_create(h, device)) != nullptr) {
         e->coarse_kind = 5;
+        return;
+    }
+    if (allow_sp2 && (e->sp2 = sp2_try_create(h, device)) != nullptr) {
+        e->coarse_kind = 6;
         return;
     }
     const bool allow_rw = !force || std::string(force) == "rw";
@@ -433,6 +442,7 @@ void destroy_fused(FusedEngine* e) {
     cudaFree(e->coarse_backup1);
     rw_destroy(e->rw);
     sp_destroy(e->sp);
+    sp2_destroy(e->sp2);
     for (void* p : e->peer_map)
         if (p) cudaIpcCloseMemHandle(p);
     cudaFree(e->xbuf);

@@ -387,6 +387,11 @@ struct SpEngine;
 SpEngine* sp_try_create(const CoarseOpH& op, int device);
 void sp_destroy(SpEngine* e);
 void launch_coarse_sp(const Params& P, const SpEngine& e, cudaStream_t st);
+// ... several 32-row blocks per warp, up to 32 blocks (coarse_sp2.cu)
+struct Sp2Engine;
+Sp2Engine* sp2_try_create(const CoarseOpH& op, int device);
+void sp2_destroy(Sp2Engine* e);
+void launch_coarse_sp2(const Params& P, const Sp2Engine& e, cudaStream_t st);
 
 bool tmem_coarse_plan(const CoarseOpH& op, TmGeom& T, std::vector<double>& spec, size_t& smem);
 void launch_coarse_tmem(const Params& P, const TmGeom& T, const double* spec, double* backup, size_t smem,

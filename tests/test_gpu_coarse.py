@@ -16,7 +16,7 @@ from cases import periodic_flags, random_field
 from paper_1309_7128_b200.api import CycleConfig, GridSpec, ScalarField, setup_jet, setup_lid_cavity
 
 pytestmark = pytest.mark.gpu
-ENGINES = {"global": 0, "smem": 1, "tmem": 2, "cl": 3, "rw": 4, "sp": 5}
+ENGINES = {"global": 0, "smem": 1, "tmem": 2, "cl": 3, "rw": 4, "sp": 5, "sp2": 6}
 
 
 @pytest.fixture(scope="module")
@@ -42,6 +42,8 @@ def level(name):
         return setup_jet(200, 600, 0.1, 8).grid, 4, False
     if name == "lid2048":  # 512 x 512: sixteen blocks (config 3's coarse level)
         return setup_lid_cavity(2048, 1000.0).grid, 4, True
+    if name == "jet4096t8":  # 512 x 1024: config 4's coarse level (32 blocks)
+        return setup_jet(4096, 8192, 0.1, 64).grid, 8, False
     raise KeyError(name)
 
 
@@ -59,8 +61,9 @@ def oracle_visit(port, w, px, py, cb, sweeps, tol, singular):
     return ce, k, rc
 
 
-@pytest.mark.parametrize("engine", ["sp", "rw", "cl", "tmem", "smem", "global"])
-@pytest.mark.parametrize("name", ["jet256", "lid256", "lid512", "jet512t8", "lid520", "jet200x600", "lid2048"])
+@pytest.mark.parametrize("engine", ["sp", "sp2", "rw", "cl", "tmem", "smem", "global"])
+@pytest.mark.parametrize("name", ["jet256", "lid256", "lid512", "jet512t8", "lid520", "jet200x600", "lid2048",
+                                  "jet4096t8"])
 @pytest.mark.parametrize("budget,first", [(1, 1), (5, 3), (37, 32), (100, 7)])
 def test_fixed_length_visit(dev, port, monkeypatch, engine, name, budget, first):
     P = dev
@@ -94,7 +97,7 @@ def test_fixed_length_visit(dev, port, monkeypatch, engine, name, budget, first)
         assert rc == rc_want
 
 
-@pytest.mark.parametrize("engine", ["sp", "rw", "cl"])
+@pytest.mark.parametrize("engine", ["sp", "sp2", "rw", "cl"])
 @pytest.mark.parametrize("name", ["jet256", "lid256", "lid512"])
 @pytest.mark.parametrize("first", [1, 4, 32])
 def test_visit_stops_at_the_reference_sweep(dev, port, monkeypatch, engine, name, first):
