@@ -511,6 +511,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and "RANK" in os.environ:
+        # NCCL's version banner goes to stdout ahead of the JSON line; keep stdout to the one line
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         import torch
         import torch.distributed as tdist
         if args.impl == "ours":  # the reference arm is CPU-only (gloo), no device needed

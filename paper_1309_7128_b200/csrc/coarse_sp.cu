@@ -95,6 +95,21 @@ namespace {
 
 extern __shared__ __align__(16) double sp_dyn[];
 
+// ISMG_SP_CHECK builds (tools/build_variant.sh): bounds of every ring slot and
+// layout diagonal, trapping on the first violation (compute-sanitizer is not
+// available on this pool).
+#ifdef ISMG_SP_CHECK
+#define SP_ASSERT(c, what)                                                                     \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("coarse_sp bounds: %s (block %d thread %d)\n", what, blockIdx.x, threadIdx.x); \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define SP_ASSERT(c, what) (void)0
+#endif
+
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -270,6 +285,8 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
             const int d = d0 + j;
 #ifndef ISMG_SPX_NOCP
             if (d + kK >= kDLo && d + kK <= dhi + kR) {  // prefetch for step t + kK
+                SP_ASSERT(d + kK - 61 + kDOff >= 0 && d + kK + 1 + kDOff < T.dspan, "prefetch diagonal");
+                SP_ASSERT(bslot(j + kK) >= 0 && bslot(j + kK) < kQB * 32, "rhs ring slot");
                 cp8(sE + 8u * uint32_t(((j + kK) & 7) * 32), pE + 32 * j);
                 cp8(sB + 8u * uint32_t(bslot(j + kK)), pB + 32 * j);
                 if (lane == 31) cp8(sX + 8u * uint32_t((j + kK) & 7), pX + 32 * j);
@@ -282,6 +299,10 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
                 // ---- update of column I (sweep g) ----
                 const int I = d - 2 * lane;
                 const bool act_u = rowok && unsigned(I) < unsigned(ncx) && d <= dhi;
+                SP_ASSERT(nslot(j - kR - 1) >= 0 && nslot(j + kD) + kRows <= kQ * kRows, "new-value ring slot");
+                SP_ASSERT(bslot(j - kR) >= 0 && bslot(j) < kQB * 32, "rhs ring slot");
+                SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
+                SP_ASSERT(!has_n || b + 1 < T.nb, "mirror target");
                 const double E = rE[(j & 7) * 32];
                 const double NE = lane < 31 ? rE[((j + 2) & 7) * 32 + 1] : rX[j & 7];
                 const double SE = rN[nslot(j - 1) + lane];

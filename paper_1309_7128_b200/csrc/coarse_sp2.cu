@@ -81,6 +81,20 @@ namespace {
 
 extern __shared__ __align__(16) double sp2_dyn[];
 
+// ISMG_SP_CHECK builds: bounds of every ring slot and layout diagonal, trapping
+// on the first violation (compute-sanitizer is not available on this pool).
+#ifdef ISMG_SP_CHECK
+#define SP_ASSERT(c, what)                                                                      \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("coarse_sp2 bounds: %s (block %d thread %d)\n", what, blockIdx.x, threadIdx.x); \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define SP_ASSERT(c, what) (void)0
+#endif
+
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -226,6 +240,8 @@ __device__ __forceinline__ void blk_step(Blk& B, int w, int b, bool rowok, int j
     double* rN = sp2_dyn + w * (kQ * kRows);
     const double* rE = sp2_dyn + M.e + w * (kQE * 32) + lane;
     const double* rB = sp2_dyn + M.bu + w * (2 * kQB * 32) + lane;
+    SP_ASSERT(nslot(j - kR - 1) >= 0 && nslot(j + kD) + kRows <= kQ * kRows, "new-value ring slot");
+    SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
     // inputs of both cells (none is written by this step)
     const double E = rE[eslot(j) * 32];
     const double NE = lane < 31 ? rE[eslot(j + 2) * 32 + 1] : sp2_dyn[M.x + w * kQE + eslot(j)];
@@ -292,6 +308,8 @@ __device__ __forceinline__ void blk_prefetch(int w, int slot, int dp, const Smem
 #ifndef ISMG_SPX_NOCP
     const int lane = threadIdx.x & 31;
     const uint32_t so = uint32_t(slot) * 256u;
+    SP_ASSERT(slot >= 0 && slot < kQE, "prefetch ring slot");
+    SP_ASSERT(dp - 61 + kDOff >= 0 && dp - kR + kDOff >= 0, "prefetch diagonal");
     cp8(su32(sp2_dyn + M.e + w * (kQE * 32) + lane) + so, xo_row + (dp + 1 + kDOff) * 32);
     cp8(su32(sp2_dyn + M.bu + w * (2 * kQB * 32) + lane) + so, bd_row + (dp + kDOff) * 32);
     cp8(su32(sp2_dyn + M.bu + w * (2 * kQB * 32) + kQB * 32 + lane) + so, bd_row + (dp - kR + kDOff) * 32);
