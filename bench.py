@@ -296,7 +296,7 @@ def run_reference_arm(args, rank, world):
                          "cpu_model": cpu_model(), "timing_rounds_wall_s": rounds_wall},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -485,11 +485,35 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def solver_coarse_cells(g, cfg):
     return ((g.nx + cfg.tile - 1) // cfg.tile) * ((g.ny + cfg.tile - 1) // cfg.tile)
+
+
+_STDOUT_FD = None  # the real stdout while libraries' banners (NCCL) are sent to stderr
+
+
+def quiet_stdout():
+    """Send fd 1 to stderr until emit(): NCCL prints its version banner on stdout
+    from C code when a communicator is created, ahead of the one JSON line."""
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    """The bench's one JSON line, on the real stdout."""
+    text = json.dumps(line) + "\n"
+    sys.stdout.flush()
+    if _STDOUT_FD is None:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    else:
+        os.write(_STDOUT_FD, text.encode())
 
 
 def main():
@@ -511,9 +535,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and "RANK" in os.environ:
-        # NCCL's version banner goes to stdout ahead of the JSON line; keep stdout to the one line
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
+        quiet_stdout()  # NCCL's version banner must not precede the JSON line
         import torch
         import torch.distributed as tdist
         if args.impl == "ours":  # the reference arm is CPU-only (gloo), no device needed

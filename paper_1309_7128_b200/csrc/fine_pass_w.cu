@@ -47,7 +47,10 @@ namespace {
 #define ISMG_FINE_MINB_PR 12
 #endif
 #ifndef ISMG_FINE_MINB_MP
-#define ISMG_FINE_MINB_MP 1  // the multi-GPU variant spills at 14
+#define ISMG_FINE_MINB_MP 1  // the multi-GPU all-phases variant spills at 14
+#endif
+#ifndef ISMG_FINE_MINB_MP_SW
+#define ISMG_FINE_MINB_MP_SW 14  // multi-GPU sweep-only kernel (PH 1): 20 B of spills; 2 GPUs at 16384^2 127.3 G against 117.1 G at 12 (all-phases kernel 111.4 G)
 #endif
 
 constexpr int kRowW = 128;  // ring row: columns [a-4, a+124)
@@ -737,15 +740,19 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
 }
 
-// PH selects the phases a kernel serves: 0 all, 2 the prolongation / residual pass
-// (prolong_w2). A single-GPU graph slot launches PH 2 then PH 0; the kernel whose
+// PH selects the phases a kernel serves: 0 all, 1 the sweep only, 2 the
+// prolongation / residual pass (prolong_w2). A single-GPU graph slot launches
+// PH 2 then PH 0; a multi-GPU slot PH 2, its exchange, PH 1, its exchange (the
+// all-phases multi-GPU kernel needs > 128 registers: 8 warps per SM). The kernel whose
 // phase it is not exits at once. The PH 0 kernel is the sweep kernel, compiled as it
 // was before the split: the sweep sits at the 128-register cap and its speed
 // follows the whole kernel's register allocation (measured: a sweep-only
 // instantiation, or any growth of the inlined prolongation, ran 142-144 against
 // 125 us per 4096^2 pass).
 template <bool MP, int PH>
-__global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : (PH == 2 ? ISMG_FINE_MINB_PR : ISMG_FINE_MINB))
+__global__ void __launch_bounds__(32, PH == 2 ? ISMG_FINE_MINB_PR
+                                              : (MP ? (PH == 1 ? ISMG_FINE_MINB_MP_SW : ISMG_FINE_MINB_MP)
+                                                    : ISMG_FINE_MINB))
     fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
@@ -756,6 +763,8 @@ __global__ void __launch_bounds__(32, MP ? ISMG_FINE_MINB_MP : (PH == 2 ? ISMG_F
     if (PH == 2) {
         if (st.phase == kProlong) prolong_w2<MP>(sm, P, st, nq, true);
         else if (st.phase == kResid) prolong_w2<MP>(sm, P, st, nq, false);
+    } else if (PH == 1) {
+        if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
     } else {
         if (st.phase == kFine) sweep_w<MP>(sm, P, st, nq);
         else if (st.phase == kProlong) prolong_w<MP>(sm, P, st, nq, true);
@@ -785,8 +794,10 @@ dim3 fine_pass_w_grid(const Params& P) {
 }
 int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only, bool ph2_only) {
     const int nq = fine_pass_w_quads(P.tile);
-    if (P.mp) {
-        fine_pass_w_kernel<true, 0><<<grid, 32, 0, st>>>(P, nq);
+    if (P.mp) {  // one kernel per call; the caller follows each with the exchange (fused_host.cu)
+        if (getenv("ISMG_MP_ALLPHASE")) fine_pass_w_kernel<true, 0><<<grid, 32, 0, st>>>(P, nq);  // A/B hook
+        else if (ph2_only) fine_pass_w_kernel<true, 2><<<grid, 32, 0, st>>>(P, nq);
+        else fine_pass_w_kernel<true, 1><<<grid, 32, 0, st>>>(P, nq);
         return 1;
     }
     if (!sweep_only) fine_pass_w_kernel<false, 2><<<grid, 32, 0, st>>>(P, nq);

@@ -168,6 +168,16 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     ISMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < slots; ++k) {
         launch_coarse(e, e.P, c.stream);
+        if (e.P.mp && e.fine_kind == 2 && !getenv("ISMG_MP_ALLPHASE")) {
+            // multi-GPU: [prolongation / residual pass, exchange, sweep pass, exchange]; the
+            // exchange after a pass that did not run (not its phase) returns at once
+            launch_fine_pass_w(e.P, e.grid, c.stream, false, true);
+            mp_exchange(e, c);
+            launch_fine_pass_w(e.P, e.grid, c.stream, true, false);
+            mp_exchange(e, c);
+            e.fine_launches = 3;  // (+1 exchange counted by the caller)
+            continue;
+        }
         e.fine_launches = launch_fine(e, c.stream);
         if (e.P.mp) mp_exchange(e, c);
     }
