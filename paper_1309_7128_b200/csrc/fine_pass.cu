@@ -344,13 +344,22 @@ void launch_finalize(const Params& P, View xuser, cudaStream_t st) {
 // every rank decides on identical values), assemble the coarse rhs from the
 // ranks' coarse rows, and apply the reference's branch logic. The next pass
 // reads its halo rows straight from the gathered packs.
+// The exchange after a multi-GPU fine pass, on every rank: wait for every
+// rank's flag of this pass, pull every rank's coarse-rhs rows from its pack slot
+// (peer memory over NVLink) into cb, then (the last CTA, by ticket) reduce the
+// pass partials in rank order (identical bits on every rank) and decide. The
+// copy is spread over kUnpackCtas CTAs: one CTA pulling the 2 MB of a 512^2
+// coarse rhs took ~125 us per pass (latency-bound NVLink loads).
+constexpr int kUnpackCtas = 32;
 __global__ void mp_unpack_kernel(Params P) {
     __shared__ int s_pass;
+    __shared__ unsigned s_last;
     Ctl* st = P.ctl;
 #ifdef ISMG_MP_TRACE
     const long long tu0 = gtimer();
 #endif
-    const unsigned long long want = st->mp_seq + 1ull;  // flag value of this slot's pass
+    const unsigned long long want = st->mp_seq + 1ull;  // flag value of this slot's pass (mp_seq changes only
+                                                         // after every CTA has passed the ticket below)
     if (threadIdx.x == 0) {
         const volatile unsigned long long* f = P.xflag[P.rank];
         int pass = f[P.rank] >= want;  // a fine pass ran in this slot (on every rank alike)
@@ -359,7 +368,7 @@ __global__ void mp_unpack_kernel(Params P) {
             for (int q = 0; q < P.nranks && pass; ++q)
                 while (f[q] < want)
                     if (gtimer() - t0 > 4000000000ll) {  // a peer is gone: stop instead of hanging
-                        st->mp_error = 1, st->phase = kDone, pass = 0;
+                        st->mp_error = 1, pass = 0;
                         break;
                     }
             __threadfence_system();
@@ -367,34 +376,51 @@ __global__ void mp_unpack_kernel(Params P) {
         s_pass = pass;
     }
     __syncthreads();
-    if (!s_pass) return;
+    if (!s_pass) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && st->mp_error == 1) st->phase = kDone;
+        return;
+    }
     const int L = P.pack_len;
     const int64_t po = int64_t((want - 1ull) & 1ull) * P.nranks * L;  // this pass's parity
-    // coarse rhs rows of every rank -> cb (used by the next coarse visit), pulled
-    // from each rank's own slot (peer memory over NVLink)
+    // coarse rhs rows of every rank -> cb (used by the next coarse visit)
+    const int nthr = int(gridDim.x * blockDim.x), tid = int(blockIdx.x * blockDim.x + threadIdx.x);
     for (int r = 0; r < P.nranks; ++r) {
         int f0, f1;
         strip_of(P.ny, P.tile, P.nranks, r, &f0, &f1);
         const int c0 = f0 / P.tile, c1 = (f1 + P.tile - 1) / P.tile;
         const double* src = P.xch[r] + po + int64_t(r) * L + 8;
         const int n = (c1 - c0) * P.ncx;
-        for (int k0 = threadIdx.x; k0 < n; k0 += 4 * blockDim.x) {
+        for (int k0 = tid; k0 < n; k0 += 4 * nthr) {
             double v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {  // four loads in flight per thread
-                const int k = k0 + u * int(blockDim.x);
+                const int k = k0 + u * nthr;
                 const int jj = k / P.ncx, I = k - jj * P.ncx;
                 v[u] = k < n ? __ldcv(src + int64_t(jj) * P.cb.pitch + I) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int k = k0 + u * int(blockDim.x);
+                const int k = k0 + u * nthr;
                 const int jj = k / P.ncx, I = k - jj * P.ncx;
                 if (k < n) P.cb.at(I, c0 + jj) = v[u];
             }
         }
     }
+    __syncthreads();
+    unsigned* ticket = P.ticket + 1 + (P.nstrips * P.nchunks + 31) / 32;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
     if (threadIdx.x == 0) {  // pass partials reduced in rank order: identical bits on every rank
+        *ticket = 0u;
+        __threadfence();
+        if (st->mp_error == 1) {
+            st->phase = kDone;
+            return;
+        }
         double m = 0.0, c = 0.0, sx = 0.0;
         for (int r = 0; r < P.nranks; ++r) {
             const double* v = P.xch[r] + po + int64_t(r) * L;
@@ -414,7 +440,7 @@ __global__ void mp_unpack_kernel(Params P) {
 #endif
     }
 }
-void launch_mp_unpack(const Params& P, cudaStream_t st) { mp_unpack_kernel<<<1, 1024, 0, st>>>(P); }
+void launch_mp_unpack(const Params& P, cudaStream_t st) { mp_unpack_kernel<<<kUnpackCtas, 512, 0, st>>>(P); }
 
 }  // namespace fz
 }  // namespace ismgb

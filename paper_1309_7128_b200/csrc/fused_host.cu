@@ -412,11 +412,11 @@ FusedEngine* make_fused(Solver& s) {
     P.w = L.d_w;
     P.ax = L.ax, P.ay = L.ay;
     const int nb = P.nstrips * P.nchunks;
-    // per-CTA partials + per-32-CTA group partials; tickets: [all, per group]
+    // per-CTA partials + per-32-CTA group partials; tickets: [all, per group, exchange (multi-GPU)]
     const int ngrp = (nb + 31) / 32;
     ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 3 * size_t(nb + ngrp)));
-    ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned) * size_t(1 + ngrp)));
-    ISMG_CUDA(cudaMemset(P.ticket, 0, sizeof(unsigned) * size_t(1 + ngrp)));
+    ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned) * size_t(2 + ngrp)));
+    ISMG_CUDA(cudaMemset(P.ticket, 0, sizeof(unsigned) * size_t(2 + ngrp)));
     P.visit_cap = int(std::min<long long>(P.max_total + 2, 1 << 22));
     ISMG_CUDA(cudaMalloc(&e->d_log, sizeof(int) * 2 * P.visit_cap));
     P.visit_log = e->d_log;
