@@ -43,9 +43,16 @@ namespace fz {
 
 namespace {
 
-constexpr int kS = 4;                  // steps between named barriers of the compute warps
+#ifndef ISMG_SP_S
+#define ISMG_SP_S 4
+#endif
+constexpr int kS = ISMG_SP_S;          // steps between named barriers of the compute warps (4 or 8)
 constexpr int kD = kS - 1;             // skew between consecutive 32-row blocks (steps)
+#ifdef ISMG_SP_INLINE_RES
 constexpr int kR = 3 + kD + kS;        // residual lag (steps): row 32's mirror value is >= kS steps old
+#else
+constexpr int kR = 0;                  // the residual is a pass over the sweep's output (no lag)
+#endif
 constexpr int kK = 5;                  // cp.async prefetch distance (steps)
 constexpr int kQ = 24;                 // new-value ring slots (3 segments of 8)
 constexpr int kQE = 8, kQB = 16;       // old-value / rhs ring slots
@@ -59,9 +66,14 @@ constexpr int kDSpanPad = 168;         // diagonals per block: ncx + kDSpanPad
 constexpr int kSpThreads = 32 * (kMaxW + 1);
 constexpr int kInf = INT_MAX;
 
+static_assert(kS == 4 || kS == 8, "barrier interval divides the 8-step iteration");
 static_assert(kK + kR + 1 <= kQB, "rhs ring: slots of the residual's rhs live until the update overwrites them");
 static_assert(kK + 1 <= kQE, "old-value ring");
+#ifdef ISMG_SP_INLINE_RES
 static_assert(kD + kR + 2 * kS <= kQ, "new-value ring: live span (mirror writes ahead, residual reads behind)");
+#else
+static_assert(kD + kS < kQ, "new-value ring: a row -1 mirror slot is read before block b-1 rewrites it");
+#endif
 static_assert(kK - 2 >= 1, "prefetch must run ahead of the NE read (t + 2)");
 
 __device__ unsigned g_sp_stuck = 0u;  // watchdog: a wait ran past 2 s
@@ -269,8 +281,8 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
                 return (seg == 0 ? sBn : (seg == -1 ? sA : sC)) + (q & 7) * kRows;
             };
             auto bslot = [&](int q) { return (((q >> 3) & 1) ? b1 : b0) + (q & 7) * 32; };
-            if ((j & 3) == 0 && avail < t + 3 + kK + kD + 4) {  // sweep g-1 far enough for the next kS steps
-                const int need = t + 3 + kK + kD + 4;
+            if ((j & 3) == 0 && avail < min(t + 3 + kK + kD + 4, T.tend + 1)) {  // sweep g-1 far enough
+                const int need = min(t + 3 + kK + kD + 4, T.tend + 1);  // (its last step: no wait for its fold)
                 if (lane == 0) {
                     const long long tw = gtimer();
                     int a;
@@ -324,13 +336,15 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
                 const double out = act_u ? q : 0.0;
                 rN[nslot(j) + lane + 1] = out;
                 if (lane == 31 && has_n) rN[kQ * kRows + nslot(j + kD)] = out;      // row -1 of the next block
+#ifdef ISMG_SP_INLINE_RES
                 if (lane == 0 && has_p) rN[nslot(j - kD) + 33 - kQ * kRows] = out;  // row 32 of the previous block
+#endif
 #ifndef ISMG_SPX_NOSTG
                 if (d <= dhi) pO[32 * j] = out;
 #endif
                 if (act_u) rsum += out;
                 seP2 = seP, seP = SE, neP2 = neP, neP = NE, outP = out;
-#ifndef ISMG_SPX_NORES
+#ifdef ISMG_SP_INLINE_RES
                 // ---- residual of column I - kR (sweep g values on all nine points) ----
                 const int Ir = I - kR;
                 const bool act_r = rowok && unsigned(Ir) < unsigned(ncx);
@@ -358,7 +372,7 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
 #ifdef ISMG_SPX_NOBAR
             if (false) {
 #else
-            if ((j & 3) == 3) {
+            if ((j % kS) == kS - 1) {
 #endif  // named barrier of the compute warps every kS steps
                 if (b == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
                 bar_compute(nthr);
@@ -370,6 +384,62 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
         }
     }
     cp_wait<0>();
+#ifndef ISMG_SP_INLINE_RES
+    // The sweep's residual (coarse_residual, the stop test) in one pass over its
+    // output buffer, off the wavefront's critical path: every compute thread takes
+    // cells in layout order (a warp reads 256 contiguous bytes per neighbour row),
+    // b - A x in the reference's order with the cell's class weights.
+    // every warp's output stores visible to the CTA, and this SM's L1 invalidated
+    // (fence.acq_rel.gpu emits CCTL.IVALL): lines of the buffer cached by an earlier
+    // sweep of this CTA must not serve the pass's L1-cached loads
+    if (threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    bar_compute(nthr);
+    const bool rowok_blk = true;
+    if (!aborted && rowok_blk) {
+        // warp b walks its block's diagonals d = 0 .. ncx + 61 (lane l: cell (d - 2l, J));
+        // lane l keeps x(d-3 .. d+3) of its row in registers, one new coalesced load
+        // per diagonal; rows J +- 1 come from lanes l +- 1 by shuffle, across the block
+        // edges from the neighbour blocks' lane 0 / 31 (zero buffer past the grid)
+        const double* Xb = xn + int64_t(b) * T.bstride + kDOff * 32 + lane;
+        const double* Bb = D.bd + int64_t(b) * T.bstride + kDOff * 32 + lane;
+        const double* Xn = (b + 1 < T.nb ? xn + int64_t(b + 1) * T.bstride : D.zero) + kDOff * 32;       // lane 0
+        const double* Xp = (b > 0 ? xn + int64_t(b - 1) * T.bstride : D.zero) + kDOff * 32 + 31;         // lane 31
+        const int span = ncx + 62;
+        double w0 = Xb[-3 * 32], w1 = Xb[-2 * 32], w2 = Xb[-32], w3 = Xb[0], w4 = Xb[32], w5 = Xb[64];
+#pragma unroll 8
+        for (int dd = 0; dd < span; ++dd) {  // (unrolled: the iterations' loads issue together)
+            const double w6 = Xb[(dd + 3) * 32];  // x(d+3)
+            const double bv = Bb[dd * 32];
+            // neighbours: lane l+1 holds row J+1 two diagonals over, lane l-1 row J-1
+            double N = __shfl_down_sync(kFull, w5, 1), NE = __shfl_down_sync(kFull, w6, 1),
+                   NW = __shfl_down_sync(kFull, w4, 1);
+            double S = __shfl_up_sync(kFull, w1, 1), SE = __shfl_up_sync(kFull, w2, 1),
+                   SW = __shfl_up_sync(kFull, w0, 1);
+            if (lane == 31 && dd >= 62) N = Xn[(dd - 62) * 32], NE = Xn[(dd - 61) * 32], NW = Xn[(dd - 63) * 32];
+            if (lane == 0 && dd < ncx) S = Xp[(dd + 62) * 32], SE = Xp[(dd + 63) * 32], SW = Xp[(dd + 61) * 32];
+            const int I = dd - 2 * lane;
+            if (rowok && unsigned(I) < unsigned(ncx)) {
+                const int cls = (J == 0 || J == T.ncy - 1) ? ring_cls[(J == 0 ? 0 : ncx) + I]
+                                                            : (I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls));
+                const double2* w = reinterpret_cast<const double2*>(tbl + 10 * cls);
+                const double2 r01 = w[0], r23 = w[1], r45 = w[2], r67 = w[3], r89 = w[4];
+                double a = r01.x * w3;
+                a += r01.y * w4;
+                a += r23.x * w2;
+                a += r23.y * N;
+                a += r45.x * S;
+                a += r45.y * NE;
+                a += r67.x * NW;
+                a += r67.y * SE;
+                a += r89.x * SW;
+                double mm = fabs(bv - a);
+                mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
+                lmax = fmax(lmax, mm);
+            }
+            w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = w5, w5 = w6;
+        }
+    }
+#endif
     // fold: max|r| (order-free), Σx in a fixed order (lanes by tree, blocks in order)
     for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(kFull, lmax, o));
     rsum = warp_sum_down(rsum);
