@@ -88,6 +88,7 @@ struct SpK {
     int ncls, ring, spec_words;
     int singular;
     int tend;                // last CTA step of a sweep
+    int nseg, seglen;        // residual chunks: nb blocks x nseg diagonal segments of seglen
 };
 
 struct SpD {
@@ -99,8 +100,13 @@ struct SpD {
     unsigned* finw;              // [B] sweep g done: finw[g % B] = g + 1
     double* resw;                // [B] residual max of sweep g
     double* sumw;                // [B] Σ x of sweep g (anchor)
-    int* st;                     // [0] first converged sweep (INT_MAX none), [1] sweeps finished
+    int* st;                     // [0] first converged sweep (INT_MAX none), [1] sweeps finished, [2] oldest
+                                 // sweep whose residual chunks may be unclaimed
     unsigned* bar;               // grid barrier: [0] arrivals, [1] generation
+    unsigned* rready;            // [B] sweep g's output complete, its residual chunks claimable: g + 1
+    unsigned* rclaim;            // [B] residual chunks claimed
+    unsigned* rdone;             // [B] residual chunks done
+    unsigned long long* rbits;   // [B] residual max so far (bits of a non-negative double: ordered as integers)
 };
 
 namespace {
@@ -199,6 +205,7 @@ struct SpShared {
     int aborted;
     int go;
     int dec[2];     // abort decision per barrier parity
+    int rs, rbase;  // residual chunks claimed: sweep, first chunk
     double wmax[kMaxW], wsum[kMaxW];
 };
 
@@ -385,60 +392,7 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     }
     cp_wait<0>();
 #ifndef ISMG_SP_INLINE_RES
-    // The sweep's residual (coarse_residual, the stop test) in one pass over its
-    // output buffer, off the wavefront's critical path: every compute thread takes
-    // cells in layout order (a warp reads 256 contiguous bytes per neighbour row),
-    // b - A x in the reference's order with the cell's class weights.
-    // every warp's output stores visible to the CTA, and this SM's L1 invalidated
-    // (fence.acq_rel.gpu emits CCTL.IVALL): lines of the buffer cached by an earlier
-    // sweep of this CTA must not serve the pass's L1-cached loads
-    if (threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    bar_compute(nthr);
-    const bool rowok_blk = true;
-    if (!aborted && rowok_blk) {
-        // warp b walks its block's diagonals d = 0 .. ncx + 61 (lane l: cell (d - 2l, J));
-        // lane l keeps x(d-3 .. d+3) of its row in registers, one new coalesced load
-        // per diagonal; rows J +- 1 come from lanes l +- 1 by shuffle, across the block
-        // edges from the neighbour blocks' lane 0 / 31 (zero buffer past the grid)
-        const double* Xb = xn + int64_t(b) * T.bstride + kDOff * 32 + lane;
-        const double* Bb = D.bd + int64_t(b) * T.bstride + kDOff * 32 + lane;
-        const double* Xn = (b + 1 < T.nb ? xn + int64_t(b + 1) * T.bstride : D.zero) + kDOff * 32;       // lane 0
-        const double* Xp = (b > 0 ? xn + int64_t(b - 1) * T.bstride : D.zero) + kDOff * 32 + 31;         // lane 31
-        const int span = ncx + 62;
-        double w0 = Xb[-3 * 32], w1 = Xb[-2 * 32], w2 = Xb[-32], w3 = Xb[0], w4 = Xb[32], w5 = Xb[64];
-#pragma unroll 8
-        for (int dd = 0; dd < span; ++dd) {  // (unrolled: the iterations' loads issue together)
-            const double w6 = Xb[(dd + 3) * 32];  // x(d+3)
-            const double bv = Bb[dd * 32];
-            // neighbours: lane l+1 holds row J+1 two diagonals over, lane l-1 row J-1
-            double N = __shfl_down_sync(kFull, w5, 1), NE = __shfl_down_sync(kFull, w6, 1),
-                   NW = __shfl_down_sync(kFull, w4, 1);
-            double S = __shfl_up_sync(kFull, w1, 1), SE = __shfl_up_sync(kFull, w2, 1),
-                   SW = __shfl_up_sync(kFull, w0, 1);
-            if (lane == 31 && dd >= 62) N = Xn[(dd - 62) * 32], NE = Xn[(dd - 61) * 32], NW = Xn[(dd - 63) * 32];
-            if (lane == 0 && dd < ncx) S = Xp[(dd + 62) * 32], SE = Xp[(dd + 63) * 32], SW = Xp[(dd + 61) * 32];
-            const int I = dd - 2 * lane;
-            if (rowok && unsigned(I) < unsigned(ncx)) {
-                const int cls = (J == 0 || J == T.ncy - 1) ? ring_cls[(J == 0 ? 0 : ncx) + I]
-                                                            : (I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls));
-                const double2* w = reinterpret_cast<const double2*>(tbl + 10 * cls);
-                const double2 r01 = w[0], r23 = w[1], r45 = w[2], r67 = w[3], r89 = w[4];
-                double a = r01.x * w3;
-                a += r01.y * w4;
-                a += r23.x * w2;
-                a += r23.y * N;
-                a += r45.x * S;
-                a += r45.y * NE;
-                a += r67.x * NW;
-                a += r67.y * SE;
-                a += r89.x * SW;
-                double mm = fabs(bv - a);
-                mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
-                lmax = fmax(lmax, mm);
-            }
-            w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = w5, w5 = w6;
-        }
-    }
+    // (the sweep's residual: chunks over the SMs after the wavefront, sp_res_chunk)
 #endif
     // fold: max|r| (order-free), Σx in a fixed order (lanes by tree, blocks in order)
     for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(kFull, lmax, o));
@@ -483,19 +437,118 @@ __device__ __forceinline__ void sp_comm(const SpD& D, SpShared& sh, int g, int P
     __syncwarp();
 }
 
+// One residual chunk of sweep g (coarse_residual, the stop test after every sweep),
+// by one warp: block bb's diagonals [d0, d1) of the sweep's output buffer. Lane l
+// keeps x(d-3 .. d+3) of its row (J = 32 bb + l) in registers, one coalesced load
+// per diagonal; rows J +- 1 come from lanes l +- 1 by shuffle and across the block
+// edges from the neighbour blocks' lane 0 / 31 (zero buffer past the grid). Class
+// weights and operation order are the update's. Returns the lanes' max |r|.
+__device__ double sp_res_chunk(const SpK& T, const SpD& D, const double* tbl, const int* ring_cls, int g, int chunk) {
+    const int lane = threadIdx.x & 31, ncx = T.ncx, ncy = T.ncy;
+    const int bb = chunk / T.nseg, sg = chunk - bb * T.nseg;
+    const int span = ncx + 62;
+    const int d0 = sg * T.seglen, d1 = min(span, d0 + T.seglen);
+    const double* xn = D.bufs + size_t(g % T.B) * T.bufsz;
+    const int J = 32 * bb + lane;
+    const bool rowok = J < ncy;
+    int wcls = T.ncls, bcls = T.ncls, ecls = T.ncls;
+    if (rowok && J != 0 && J != ncy - 1) wcls = ring_cls[2 * ncx + J], ecls = ring_cls[2 * ncx + ncy + J];
+    const double* Xb = xn + int64_t(bb) * T.bstride + kDOff * 32 + lane;
+    const double* Bb = D.bd + int64_t(bb) * T.bstride + kDOff * 32 + lane;
+    const double* Xn = (bb + 1 < T.nb ? xn + int64_t(bb + 1) * T.bstride : D.zero) + kDOff * 32;      // lane 0
+    const double* Xp = (bb > 0 ? xn + int64_t(bb - 1) * T.bstride : D.zero) + kDOff * 32 + 31;        // lane 31
+    double lmax = 0.0;
+    if (d0 >= d1) return lmax;
+    double w0 = Xb[(d0 - 3) * 32], w1 = Xb[(d0 - 2) * 32], w2 = Xb[(d0 - 1) * 32], w3 = Xb[d0 * 32],
+           w4 = Xb[(d0 + 1) * 32], w5 = Xb[(d0 + 2) * 32];
+#pragma unroll 4
+    for (int dd = d0; dd < d1; ++dd) {
+        const double w6 = Xb[(dd + 3) * 32];  // x(d+3)
+        const double bv = Bb[dd * 32];
+        double N = __shfl_down_sync(kFull, w5, 1), NE = __shfl_down_sync(kFull, w6, 1),
+               NW = __shfl_down_sync(kFull, w4, 1);
+        double S = __shfl_up_sync(kFull, w1, 1), SE = __shfl_up_sync(kFull, w2, 1),
+               SW = __shfl_up_sync(kFull, w0, 1);
+        if (lane == 31 && dd >= 62) N = Xn[(dd - 62) * 32], NE = Xn[(dd - 61) * 32], NW = Xn[(dd - 63) * 32];
+        if (lane == 0 && dd < ncx) S = Xp[(dd + 62) * 32], SE = Xp[(dd + 63) * 32], SW = Xp[(dd + 61) * 32];
+        const int I = dd - 2 * lane;
+        if (rowok && unsigned(I) < unsigned(ncx)) {
+            const int cls = (J == 0 || J == ncy - 1) ? ring_cls[(J == 0 ? 0 : ncx) + I]
+                                                      : (I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls));
+            const double2* w = reinterpret_cast<const double2*>(tbl + 10 * cls);
+            const double2 r01 = w[0], r23 = w[1], r45 = w[2], r67 = w[3], r89 = w[4];
+            double a = r01.x * w3;
+            a += r01.y * w4;
+            a += r23.x * w2;
+            a += r23.y * N;
+            a += r45.x * S;
+            a += r45.y * NE;
+            a += r67.x * NW;
+            a += r67.y * SE;
+            a += r89.x * SW;
+            double mm = fabs(bv - a);
+            mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
+            lmax = fmax(lmax, mm);
+        }
+        w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = w5, w5 = w6;
+    }
+    return lmax;
+}
+
+// thread 0: claim up to `want` residual chunks of the oldest sweep that has some
+// unclaimed (sweeps publish rready in order). Returns the sweep (or -1), *base the
+// first chunk claimed.
+__device__ int sp_claim(const SpK& T, const SpD& D, int want, int* base) {
+    const int nchunk = T.nb * T.nseg;
+    for (int tries = 0; tries < 4; ++tries) {
+        const int s = ld_rlx_gpu(D.st + 2);
+        if (ld_acq_gpu(D.rready + s % T.B) != unsigned(s + 1)) return -1;  // not published (yet)
+        const unsigned c = atomicAdd(D.rclaim + s % T.B, unsigned(want));
+        if (c < unsigned(nchunk)) {
+            *base = int(c);
+            return s;
+        }
+        atomicCAS(D.st + 2, s, s + 1);  // every chunk of s claimed: move on
+    }
+    return -1;
+}
+
+// every compute warp takes one chunk of sweep s (chunks base .. base + nw - 1); the
+// warp that completes the sweep's last chunk decides it: residual, stop, done.
+__device__ void sp_res_work(const SpK& T, const SpD& D, const Params& P, const double* tbl, const int* ring_cls,
+                            int s, int base) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nchunk = T.nb * T.nseg;
+    const int chunk = base + w;
+    if (s < 0 || w >= T.nb || chunk >= nchunk) return;
+    double m = sp_res_chunk(T, D, tbl, ring_cls, s, chunk);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) {
+        atomicMax(D.rbits + s % T.B, (unsigned long long)__double_as_longlong(m));
+        __threadfence();
+        if (atomicAdd(D.rdone + s % T.B, 1u) == unsigned(nchunk - 1)) {  // the sweep's last chunk
+            __threadfence();
+            const double res = __longlong_as_double((long long)ld_acq_gpu(D.rbits + s % T.B));
+            D.resw[s % T.B] = res;
+            if (!(res > P.tol_coarse)) atomicMin(D.st, s);
+            __threadfence();
+            st_rel_gpu(D.finw + s % T.B, unsigned(s + 1));
+            atomicAdd(D.st + 1, 1);
+        }
+    }
+}
+
 // thread 0: may sweep g start? 1 go, 0 stop (past the first converged sweep or the budget)
 __device__ int sp_start(const SpK& T, const SpD& D, int g, long long budget, int a0) {
-    const long long t0 = gtimer();
-    for (;;) {
-        if (g >= budget || g > ld_rlx_gpu(D.st)) return 0;
-        bool ok = g < a0 + 2 * ld_rlx_gpu(D.st + 1);  // at most a0 + 2 x (sweeps finished) in flight
-        if (ok && g >= T.B)  // buffer g % B: sweep g-B decided, sweep g-B+1 done reading it
-            ok = ld_acq_gpu(D.finw + g % T.B) == unsigned(g - T.B + 1) &&
-                 ld_acq_gpu(D.finw + (g + 1) % T.B) == unsigned(g - T.B + 2);
-        if (ok) return g > ld_rlx_gpu(D.st) ? 0 : 1;
-        __nanosleep(64);
-        if (timed_out(t0)) return 0;
-    }
+    if (g > ld_rlx_gpu(D.st)) return 0;
+    if (g >= budget)  // no sweep to run: help until the sweeps below the budget have every chunk claimed
+        return ld_rlx_gpu(D.st + 2) >= budget ? 0 : 2;
+    bool ok = g < a0 + 2 * ld_rlx_gpu(D.st + 1);  // at most a0 + 2 x (sweeps finished) in flight
+    if (ok && g >= T.B)  // buffer g % B: sweep g-B decided, sweep g-B+1 done reading it
+        ok = ld_acq_gpu(D.finw + g % T.B) == unsigned(g - T.B + 1) &&
+             ld_acq_gpu(D.finw + (g + 1) % T.B) == unsigned(g - T.B + 2);
+    if (ok) return g > ld_rlx_gpu(D.st) ? 0 : 1;
+    return 2;  // wait (and help with residual chunks)
 }
 
 __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK T, SpD D) {
@@ -519,8 +572,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
     const unsigned nthreads = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.x == 0) {  // per-visit state (nobody else touches it before the barrier)
         for (int k = threadIdx.x; k < T.P; k += blockDim.x) D.prog[k] = 0ull;
-        for (int k = threadIdx.x; k < T.B; k += blockDim.x) D.finw[k] = 0u;
-        if (threadIdx.x == 0) D.st[0] = kInf, D.st[1] = 0;
+        for (int k = threadIdx.x; k < T.B; k += blockDim.x) D.finw[k] = 0u, D.rready[k] = 0u;
+        if (threadIdx.x == 0) D.st[0] = kInf, D.st[1] = 0, D.st[2] = 0;
     }
     for (int k = threadIdx.x; k < T.spec_words; k += blockDim.x) tbl[k] = D.spec[k];
     for (int k = threadIdx.x; k < NW * kQ * kRows; k += blockDim.x) ringN[k] = 0.0;  // rows -1 / 32 at the grid edge stay 0
@@ -539,8 +592,27 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
     long long steps = 0;
     if (run) {
         for (int g = blockIdx.x;; g += gridDim.x) {
+            // until sweep g may start: help with residual chunks of finished sweeps
+            const long long tw = gtimer();
+            for (;;) {
+                if (threadIdx.x == 0) {
+                    sh.go = sp_start(T, D, g, budget, a0);
+                    sh.rs = -1;
+                    if (sh.go == 2) {
+                        int base = 0;
+                        sh.rs = sp_claim(T, D, NW, &base);
+                        sh.rbase = base;
+                        if (sh.rs >= 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // also drops stale L1 lines
+                        else if (timed_out(tw)) sh.go = 0;
+                    }
+                }
+                __syncthreads();
+                if (sh.go != 2) break;
+                if (sh.rs >= 0) sp_res_work(T, D, P, tbl, ring_cls, sh.rs, sh.rbase);
+                else if (threadIdx.x == 0) __nanosleep(64);
+                __syncthreads();
+            }
             if (threadIdx.x == 0) {
-                sh.go = sp_start(T, D, g, budget, a0);
                 sh.avail = g == 0 ? kInf : 0, sh.abort_ = 0, sh.done_t = 0, sh.end = 0, sh.aborted = 0;
                 sh.dec[0] = sh.dec[1] = 0;
             }
@@ -551,18 +623,35 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
             if (warp == NW) sp_comm(D, sh, g, T.P);
             else sp_sweep(T, D, sh, ringN, ringE, ringB, ringX, tbl, ring_cls, xo, xn, g);
             __syncthreads();
-            if (threadIdx.x == 0 && !sh.aborted) {
-                double res = 0.0, sum = 0.0;
-                for (int w = 0; w < NW; ++w) res = fmax(res, sh.wmax[w]);
-                for (int w = 0; w < NW; ++w) sum += sh.wsum[w];
-                D.resw[g % T.B] = res, D.sumw[g % T.B] = sum;
-                if (!(res > P.tol_coarse)) atomicMin(D.st, g);
-                __threadfence();
-                st_rel_gpu(D.finw + g % T.B, unsigned(g + 1));
-                atomicAdd(D.st + 1, 1);
+            if (threadIdx.x == 0 && !sh.aborted) {  // publish the sweep's residual chunks
+                double sum = 0.0;
+                for (int w = 0; w < NW; ++w) sum += sh.wsum[w];  // blocks in order
+                D.sumw[g % T.B] = sum;
+                D.rbits[g % T.B] = 0ull, D.rclaim[g % T.B] = 0u, D.rdone[g % T.B] = 0u;
+                __threadfence();  // the sweep's output (every warp's stores: the CTA barrier above) first
+                st_rel_gpu(D.rready + g % T.B, unsigned(g + 1));
+                // the whole sweep to its consumer (the comm warp may have left before the last step's count)
                 st_rel_gpu(D.prog + blockIdx.x, ((unsigned long long)(unsigned)g << 32) | 0xffffffffull);
             }
             __syncthreads();
+            // work on this sweep's residual until every chunk is claimed (helpers take the rest)
+            if (!sh.aborted) {
+                for (;;) {
+                    if (threadIdx.x == 0) {
+                        int base = 0;
+                        const int s2 = sp_claim(T, D, NW, &base);
+                        sh.rs = s2, sh.rbase = base;
+                        if (s2 >= 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        // done when this sweep's chunks are all claimed
+                        sh.go = (s2 < 0 || s2 > g) ? 0 : 1;
+                    }
+                    __syncthreads();
+                    if (sh.rs >= 0) sp_res_work(T, D, P, tbl, ring_cls, sh.rs, sh.rbase);  // whatever was claimed
+                    const bool more = sh.go;
+                    __syncthreads();
+                    if (!more) break;
+                }
+            }
         }
     }
     sp_grid_sync(D.bar, gridDim.x);
@@ -647,6 +736,8 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     T.spec_words = int(S.spec.size());
     T.singular = op.singular ? 1 : 0;
     T.tend = (op.ncx + kDHiPad + kR - kDLo) + kStride * (nb - 1);
+    T.nseg = 8;  // residual chunks per block: 8 segments of the block's ncx + 62 diagonals
+    T.seglen = (op.ncx + 62 + T.nseg - 1) / T.nseg;
     const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * 32 + kQB * 32 + kQE) + S.spec.size());
     ISMG_CUDA(cudaFuncSetAttribute(coarse_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0, sms = 0;
@@ -661,7 +752,8 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     e->smem = smem;
     const size_t bufb = sizeof(double) * size_t(T.bufsz);
     const size_t bytes = bufb * size_t(T.B + 2) + sizeof(double) * S.spec.size() + sizeof(unsigned long long) * P +
-                         sizeof(unsigned) * T.B + 2 * sizeof(double) * T.B + 64 + 1024;
+                         sizeof(unsigned) * T.B + 2 * sizeof(double) * T.B + 64 + 1024 +
+                         3 * sizeof(unsigned) * T.B + sizeof(unsigned long long) * T.B + 64;
     ISMG_CUDA(cudaMalloc(&e->mem, bytes));
     ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
     char* p = static_cast<char*>(e->mem);
@@ -677,6 +769,11 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     e->D.finw = reinterpret_cast<unsigned*>(p), p += sizeof(unsigned) * T.B;
     p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 63) & ~uintptr_t(63));
     e->D.st = reinterpret_cast<int*>(p), p += 64;
+    e->D.rready = reinterpret_cast<unsigned*>(p), p += sizeof(unsigned) * T.B;
+    e->D.rclaim = reinterpret_cast<unsigned*>(p), p += sizeof(unsigned) * T.B;
+    e->D.rdone = reinterpret_cast<unsigned*>(p), p += sizeof(unsigned) * T.B;
+    p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    e->D.rbits = reinterpret_cast<unsigned long long*>(p), p += sizeof(unsigned long long) * T.B;
     e->D.bar = reinterpret_cast<unsigned*>(p);
     return e;
 }
