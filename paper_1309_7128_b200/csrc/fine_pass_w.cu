@@ -624,6 +624,26 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     same[0] = false;
 #pragma unroll
     for (int q = 1; q < 4; ++q) same[q] = I0[q] == I0[q - 1] && I1[q] == I1[q - 1];
+#ifndef ISMG_PH2_NOFAST
+    // The fast row body (uniform power-of-two tiles, the whole interior of a
+    // config-3 grid): every in-domain column of the lane has a power-of-two extent
+    // and the quad's coarse pair, so the column weights can carry 1/dx and the
+    // row weights 1/dy. Scaling by a power of two is exact, so
+    //   ((dx-s)/dx) ((dy-t)/dy c00 + t/dy c01) + ...   ==   (...) / (dx dy)
+    // bit for bit (as long as no product is subnormal), with 5 instead of 10
+    // fp64 operations per cell and no per-cell reciprocal product.
+    bool lok = true;
+    double ar[4], sr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        ar[q] = (dxq[q] - sq[q]) * idx[q], sr[q] = sq[q] * idx[q];
+        if (prolong && L.dom[q]) lok = lok && idx[q] != 0.0 && (q == 0 || same[q]);
+    }
+    bool fast = __all_sync(kFull, lok);
+#else
+    bool fast = false;
+    double ar[4] = {0, 0, 0, 0}, sr[4] = {0, 0, 0, 0};
+#endif
     const int kfirst = G.r0 - 1, klast = G.r1;
     if ((threadIdx.x & 31) == 0) {
         for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
@@ -648,13 +668,27 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     __shared__ int s_ak0[kAxRows], s_ak1[kAxRows];
     const bool tab = prolong && klast - kfirst + 2 <= kAxRows;
     if (tab) {
+        bool rok = true;  // every row of the chunk has a power-of-two extent
+        for (int i = int(threadIdx.x & 31); i < klast - kfirst + 2; i += 32) {
+            const int k = kfirst + i;
+            if (k >= 0 && k < G.ny) rok = rok && is_pow2(P.ay.dk[k]);
+        }
+        fast = __all_sync(kFull, rok) && fast;
         for (int i = int(threadIdx.x & 31); i < klast - kfirst + 2; i += 32) {
             const int k = kfirst + i;
             const bool in = k >= 0 && k < G.ny;
-            s_at[i] = in ? P.ay.t[k] : 0.0, s_adk[i] = in ? P.ay.dk[k] : 1.0;
+            const double t = in ? P.ay.t[k] : 0.0, dk = in ? P.ay.dk[k] : 1.0;
+            if (fast) {  // the row weights (dy - t) / dy and t / dy, exact
+                const double idk = pow2_recip(dk);
+                s_at[i] = (dk - t) * idk, s_adk[i] = t * idk;
+            } else {
+                s_at[i] = t, s_adk[i] = dk;
+            }
             s_ak0[i] = in ? P.ay.k0[k] : 0, s_ak1[i] = in ? P.ay.k1[k] : 0;
         }
         __syncwarp();
+    } else {
+        fast = false;
     }
     auto row_axis = [&](int k, double& t_, double& d_, int& j0_, int& j1_) {
         t_ = 0.0, d_ = 1.0, j0_ = 0, j1_ = 0;
@@ -748,8 +782,9 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     for (int s2 = 0; s2 < 4; ++s2)
 #pragma unroll
         for (int q = 0; q < 4; ++q) xw[s2][q] = bw[s2][q] = 0.0;
-    auto row = [&](auto u, int k) {
+    auto row = [&](auto u, auto fastc, int k) {
         constexpr int U = decltype(u)::value, U1 = (U + 3) & 3, U2 = (U + 2) & 3;
+        constexpr bool FAST = decltype(fastc)::value;
         const double tt = tt_n, dy = dy_n;
         const int J0 = J0_n, J1 = J1_n;
         row_axis(k + 1, tt_n, dy_n, J0_n, J1_n);
@@ -758,7 +793,24 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
             cJ0 = J0, cJ1 = J1;
         }
         mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
-        {
+        if constexpr (FAST) {  // tt, dy hold the scaled row weights t / dy, (dy - t) / dy
+            const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
+            const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
+            const double2 c01v = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+            const double2 c23v = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+            const double raw[4] = {v01.x, v01.y, v23.x, v23.y};
+            bw[U][0] = c01v.x, bw[U][1] = c01v.y, bw[U][2] = c23v.x, bw[U][3] = c23v.y;
+            const double ca = tt * c00 + dy * c01, cb = tt * c10 + dy * c11;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xw[U][q] = (raw[q] + G.c) + (ar[q] * ca + sr[q] * cb);
+            if (k < 0 || k >= G.ny || L.frozen) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xw[U][q] = 0.0;
+            } else if (L.spec) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xw[U][q] = L.dom[q] ? xw[U][q] : 0.0;
+            }
+        } else {
             const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
             const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
             const double2 c01v = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
@@ -791,14 +843,21 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
         const double W1 = sh_up(xw[U1][3]), E1 = sh_dn(xw[U1][0]);
         const int j = k - 1;
         if (L.owned && j >= G.r0 && j < G.r1) {
-            const double dr = row_part(G, j);
             double r[4];
-            r[0] = bw[U1][0] - ((((W1 + xw[U1][1]) + xw[U2][0]) + xw[U][0]) - (L.dc[0] + dr) * xw[U1][0]);
-            r[1] = bw[U1][1] - ((((xw[U1][0] + xw[U1][2]) + xw[U2][1]) + xw[U][1]) - (L.dc[1] + dr) * xw[U1][1]);
-            r[2] = bw[U1][2] - ((((xw[U1][1] + xw[U1][3]) + xw[U2][2]) + xw[U][2]) - (L.dc[2] + dr) * xw[U1][2]);
-            r[3] = bw[U1][3] - ((((xw[U1][2] + E1) + xw[U2][3]) + xw[U][3]) - (L.dc[3] + dr) * xw[U1][3]);
+            if (!FAST || (j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                r[0] = bw[U1][0] - ((((W1 + xw[U1][1]) + xw[U2][0]) + xw[U][0]) - (L.dc[0] + dr) * xw[U1][0]);
+                r[1] = bw[U1][1] - ((((xw[U1][0] + xw[U1][2]) + xw[U2][1]) + xw[U][1]) - (L.dc[1] + dr) * xw[U1][1]);
+                r[2] = bw[U1][2] - ((((xw[U1][1] + xw[U1][3]) + xw[U2][2]) + xw[U][2]) - (L.dc[2] + dr) * xw[U1][2]);
+                r[3] = bw[U1][3] - ((((xw[U1][2] + E1) + xw[U2][3]) + xw[U][3]) - (L.dc[3] + dr) * xw[U1][3]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+                for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            } else {  // interior cells of an interior row: d = 4 (col_diag + row_part, exact)
+                r[0] = bw[U1][0] - ((((W1 + xw[U1][1]) + xw[U2][0]) + xw[U][0]) - 4.0 * xw[U1][0]);
+                r[1] = bw[U1][1] - ((((xw[U1][0] + xw[U1][2]) + xw[U2][1]) + xw[U][1]) - 4.0 * xw[U1][1]);
+                r[2] = bw[U1][2] - ((((xw[U1][1] + xw[U1][3]) + xw[U2][2]) + xw[U][2]) - 4.0 * xw[U1][2]);
+                r[3] = bw[U1][3] - ((((xw[U1][2] + E1) + xw[U2][3]) + xw[U][3]) - 4.0 * xw[U1][3]);
+            }
             const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
             A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
             A.sx = A.sx + ((xw[U1][0] + xw[U1][1]) + (xw[U1][2] + xw[U1][3]));
@@ -811,12 +870,16 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
             issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     };
-    for (int kb = kfirst; kb <= klast; kb += 4) {
-        row(std::integral_constant<int, 0>{}, kb);
-        if (kb + 1 <= klast) row(std::integral_constant<int, 1>{}, kb + 1);
-        if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, kb + 2);
-        if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, kb + 3);
-    }
+    auto rows = [&](auto fastc) {
+        for (int kb = kfirst; kb <= klast; kb += 4) {
+            row(std::integral_constant<int, 0>{}, fastc, kb);
+            if (kb + 1 <= klast) row(std::integral_constant<int, 1>{}, fastc, kb + 1);
+            if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, fastc, kb + 2);
+            if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, fastc, kb + 3);
+        }
+    };
+    if (fast) rows(std::true_type{});
+    else rows(std::false_type{});
 #endif
     if (MP) mp_push(P, L, G, mpp, prolong ? G.outp : xin + L.c0);
     warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
