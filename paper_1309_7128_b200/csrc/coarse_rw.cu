@@ -905,7 +905,7 @@ RwEngine* rw_create(const RwPlan& plan) {
     const size_t bytes = 2 * mail + sizeof(unsigned long long) * kMaxG + 64 + sizeof(double) * (T.nw + 2) +
                          sizeof(double) * plan.endw.size() + sizeof(unsigned long long) * T.nw + 256;
     ISMG_CUDA(cudaMalloc(&e->mem, bytes));
-    ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
+    ISMG_ZERO(e->mem, bytes);
     char* p = static_cast<char*>(e->mem);
     e->D.ms = reinterpret_cast<uint4*>(p);
     p += mail;
@@ -920,12 +920,12 @@ RwEngine* rw_create(const RwPlan& plan) {
     e->D.dec = reinterpret_cast<double*>(p);
     p += sizeof(double) * 2;
     double* endw = reinterpret_cast<double*>(p);
-    ISMG_CUDA(cudaMemcpy(endw, plan.endw.data(), sizeof(double) * plan.endw.size(), cudaMemcpyHostToDevice));
+    ISMG_H2D(endw, plan.endw.data(), sizeof(double) * plan.endw.size());
     p += sizeof(double) * plan.endw.size();
     e->D.prog = reinterpret_cast<unsigned long long*>(p);
     e->D.endw = endw;
     const unsigned base0 = 16u;  // tags start above the zeroed mailboxes' 0
-    ISMG_CUDA(cudaMemcpy(e->D.bar + 2, &base0, sizeof(unsigned), cudaMemcpyHostToDevice));
+    ISMG_H2D(e->D.bar + 2, &base0, sizeof(unsigned));
     return e;
 }
 

@@ -56,6 +56,7 @@ constexpr int kR = 0;                  // the residual is a pass over the sweep'
 constexpr int kK = 5;                  // cp.async prefetch distance (steps)
 constexpr int kQ = 24;                 // new-value ring slots (3 segments of 8)
 constexpr int kQE = 8, kQB = 16;       // old-value / rhs ring slots
+constexpr int kEW = 33;                // old-value ring row: lanes 0..31 + row 32 (the next block's row 0, lane 31's NE)
 constexpr int kRows = 34;              // ring rows: block rows -1 .. 32
 constexpr int kMaxW = 16;              // compute warps (32-row blocks)
 constexpr int kStride = 64 + kD;       // CTA steps between consecutive blocks
@@ -76,7 +77,11 @@ static_assert(kD + kS < kQ, "new-value ring: a row -1 mirror slot is read before
 #endif
 static_assert(kK - 2 >= 1, "prefetch must run ahead of the NE read (t + 2)");
 
-__device__ unsigned g_sp_stuck = 0u;  // watchdog: a wait ran past 2 s
+__device__ unsigned g_sp_stuck = 0u;
+#ifdef ISMG_SP_TRACE  // phase clock of CTA 0 (ns, accumulated): setup, sweep 0, loop rest, grid sync, write-out, visits
+__device__ unsigned long long g_sp_trace[6];
+#define SP_TRACE(i, t) (g_sp_trace[i] += (unsigned long long)(t))
+#endif  // watchdog: a wait ran past 2 s
 
 }  // namespace
 
@@ -231,7 +236,7 @@ __device__ __forceinline__ double div_full(double num, double w, double y) {
 // update (weights of the cell's class from the table: west column, row body,
 // east column), the residual kR columns behind, a named barrier every kS steps.
 __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& sh, double* ringN, double* ringE,
-                                         double* ringB, double* ringX, const double* tbl, const int* ring_cls,
+                                         double* ringB, const double* tbl, const int* ring_cls,
                                          const double* __restrict__ xo, double* __restrict__ xn, int g) {
     const int b = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nthr = 32 * T.nb;
@@ -251,10 +256,9 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     }
     // rings of this warp (new values: [kQ][kRows]; the neighbour blocks' rings sit kQ kRows doubles away)
     double* rN = ringN + size_t(b) * kQ * kRows;
-    double* rE = ringE + size_t(b) * kQE * 32 + lane;
+    double* rE = ringE + size_t(b) * kQE * kEW + lane;
     double* rB = ringB + size_t(b) * kQB * 32 + lane;
-    double* rX = ringX + size_t(b) * kQE;
-    const uint32_t sE = su32(rE), sB = su32(rB), sX = su32(rX);
+    const uint32_t sE = su32(rE), sB = su32(rB);
     const bool has_n = b + 1 < T.nb, has_p = b > 0;
     const double* xo_b = xo + size_t(b) * T.bstride + lane;
     const double* xo_n = (has_n ? xo + size_t(b + 1) * T.bstride : D.zero);  // row 32 (b+1) = next block's lane 0
@@ -270,6 +274,23 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     bool aborted = false;
     const int mend = T.tend >> 3;
     for (int m = -1; m <= mend && !aborted; ++m) {
+#ifndef ISMG_SP_NOIDLE
+        // a group of 8 steps with neither a prefetch nor an update for this block (before or
+        // after its diagonal window): only the barriers. Idle warps otherwise issue ~30
+        // instructions per step, taking issue slots from the active warps on their SMSP.
+        if (8 * m + kDLo - kStride * b + 7 + kK < kDLo || 8 * m + kDLo - kStride * b > dhi + kR) {
+#pragma unroll
+            for (int j = kS - 1; j < 8; j += kS) {
+                if (b == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
+                bar_compute(nthr);
+                if (b == 0 && lane == 0) st_rel_cta(&sh.done_t, max(0, 8 * m + j + 1));
+                aborted = ld_vol_s(&sh.dec[h & 1]) != 0;
+                ++h;
+                if (aborted) break;
+            }
+            continue;
+        }
+#endif
         // new-value ring segments (8 slots each) of steps 8(m-1).., 8m.., 8(m+1).. (= 8(m-2)..)
         const int m3 = (m + 3) % 3;
         const int sA = ((m3 + 2) % 3) * 8 * kRows, sBn = m3 * 8 * kRows, sC = ((m3 + 1) % 3) * 8 * kRows;
@@ -306,9 +327,10 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
             if (d + kK >= kDLo && d + kK <= dhi + kR) {  // prefetch for step t + kK
                 SP_ASSERT(d + kK - 61 + kDOff >= 0 && d + kK + 1 + kDOff < T.dspan, "prefetch diagonal");
                 SP_ASSERT(bslot(j + kK) >= 0 && bslot(j + kK) < kQB * 32, "rhs ring slot");
-                cp8(sE + 8u * uint32_t(((j + kK) & 7) * 32), pE + 32 * j);
+                cp8(sE + 8u * uint32_t(((j + kK) & 7) * kEW), pE + 32 * j);
                 cp8(sB + 8u * uint32_t(bslot(j + kK)), pB + 32 * j);
-                if (lane == 31) cp8(sX + 8u * uint32_t((j + kK) & 7), pX + 32 * j);
+                // lane 31: row 32 into position 32 of the slot its NE read of step t + kK uses
+                if (lane == 31) cp8(sE + 8u * uint32_t(((j + kK + 2) & 7) * kEW + 1), pX + 32 * j);
             }
 #endif
             cp_commit();
@@ -322,8 +344,8 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
                 SP_ASSERT(bslot(j - kR) >= 0 && bslot(j) < kQB * 32, "rhs ring slot");
                 SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
                 SP_ASSERT(!has_n || b + 1 < T.nb, "mirror target");
-                const double E = rE[(j & 7) * 32];
-                const double NE = lane < 31 ? rE[((j + 2) & 7) * 32 + 1] : rX[j & 7];
+                const double E = rE[(j & 7) * kEW];
+                const double NE = rE[((j + 2) & 7) * kEW + 1];  // lane 31: position 32
                 const double SE = rN[nslot(j - 1) + lane];
                 const double bu = rB[bslot(j)];
                 const double2* wu = reinterpret_cast<const double2*>(
@@ -558,12 +580,11 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
     __shared__ SpShared sh;
     const int NW = T.nb;
     const int warp = threadIdx.x >> 5;
-    // shared memory: new-value rings [NW][kQ][kRows] | old [NW][kQE][32] | rhs [NW][kQB][32] | X [NW][kQE] | table
+    // shared memory: new-value rings [NW][kQ][kRows] | old [NW][kQE][kEW] | rhs [NW][kQB][32] | table
     double* ringN = sp_dyn;
     double* ringE = ringN + size_t(NW) * kQ * kRows;
-    double* ringB = ringE + size_t(NW) * kQE * 32;
-    double* ringX = ringB + size_t(NW) * kQB * 32;
-    double* tbl = ringX + size_t(NW) * kQE;
+    double* ringB = ringE + size_t(NW) * kQE * kEW;
+    double* tbl = ringB + size_t(NW) * kQB * 32;
     const int* ring_cls = reinterpret_cast<const int*>(tbl + 10 * (T.ncls + 1));
     const double rc0 = st->rc;  // max|cb|, formed by the fine pass that restricted
     const long long budget = P.max_total - st->total;
@@ -588,6 +609,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
         }
     }
     sp_grid_sync(D.bar, gridDim.x);  // everyone has read Ctl; rhs and state ready
+#ifdef ISMG_SP_TRACE
+    long long tr1 = gtimer(), tr2 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) SP_TRACE(0, tr1 - t_start), SP_TRACE(5, 1);
+#endif
     const int a0 = 2 * max(1, pred) + 2;
     long long steps = 0;
     if (run) {
@@ -621,8 +646,11 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
             const double* xo = g == 0 ? D.zero : D.bufs + size_t((g - 1) % T.B) * T.bufsz;
             double* xn = D.bufs + size_t(g % T.B) * T.bufsz;
             if (warp == NW) sp_comm(D, sh, g, T.P);
-            else sp_sweep(T, D, sh, ringN, ringE, ringB, ringX, tbl, ring_cls, xo, xn, g);
+            else sp_sweep(T, D, sh, ringN, ringE, ringB, tbl, ring_cls, xo, xn, g);
             __syncthreads();
+#ifdef ISMG_SP_TRACE
+            if (g == 0 && threadIdx.x == 0) tr2 = gtimer(), SP_TRACE(1, tr2 - tr1);
+#endif
             if (threadIdx.x == 0 && !sh.aborted) {  // publish the sweep's residual chunks
                 double sum = 0.0;
                 for (int w = 0; w < NW; ++w) sum += sh.wsum[w];  // blocks in order
@@ -654,7 +682,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
             }
         }
     }
+#ifdef ISMG_SP_TRACE
+    const long long tr3 = gtimer();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && tr2) SP_TRACE(2, tr3 - tr2);
+#endif
     sp_grid_sync(D.bar, gridDim.x);
+#ifdef ISMG_SP_TRACE
+    const long long tr4 = gtimer();
+    if (blockIdx.x == 0 && threadIdx.x == 0) SP_TRACE(3, tr4 - tr3);
+#endif
     int done = 0;
     double rc = rc0, sum = 0.0;
     const double* xk = nullptr;
@@ -681,6 +717,9 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
         }
         P.ce.at(I, J) = v;
     }
+#ifdef ISMG_SP_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0) SP_TRACE(4, gtimer() - tr4);
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->coarse_launches += 1;
         st->coarse_ns += gtimer() - t_start;
@@ -706,6 +745,17 @@ __global__ void __launch_bounds__(kSpThreads, 1) coarse_sp_kernel(Params P, SpK 
 
 }  // namespace
 
+#ifdef ISMG_SP_TRACE
+}  // namespace fz
+}  // namespace ismgb
+extern "C" __attribute__((visibility("default"))) void ismg_debug_sp_trace(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, ismgb::fz::g_sp_trace, sizeof(unsigned long long) * 6);
+    const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(ismgb::fz::g_sp_trace, z, sizeof(z));
+}
+namespace ismgb {
+namespace fz {
+#endif
 struct SpEngine {
     SpK T{};
     SpD D{};
@@ -738,7 +788,7 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     T.tend = (op.ncx + kDHiPad + kR - kDLo) + kStride * (nb - 1);
     T.nseg = 8;  // residual chunks per block: 8 segments of the block's ncx + 62 diagonals
     T.seglen = (op.ncx + 62 + T.nseg - 1) / T.nseg;
-    const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * 32 + kQB * 32 + kQE) + S.spec.size());
+    const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * kEW + kQB * 32) + S.spec.size());
     ISMG_CUDA(cudaFuncSetAttribute(coarse_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0, sms = 0;
     ISMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_sp_kernel, 32 * (nb + 1), smem));
@@ -755,13 +805,13 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
                          sizeof(unsigned) * T.B + 2 * sizeof(double) * T.B + 64 + 1024 +
                          3 * sizeof(unsigned) * T.B + sizeof(unsigned long long) * T.B + 64;
     ISMG_CUDA(cudaMalloc(&e->mem, bytes));
-    ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
+    ISMG_ZERO(e->mem, bytes);
     char* p = static_cast<char*>(e->mem);
     e->D.bufs = reinterpret_cast<double*>(p), p += bufb * T.B;
     e->D.zero = reinterpret_cast<double*>(p), p += bufb;
     e->D.bd = reinterpret_cast<double*>(p), p += bufb;
     double* spec = reinterpret_cast<double*>(p);
-    ISMG_CUDA(cudaMemcpy(spec, S.spec.data(), sizeof(double) * S.spec.size(), cudaMemcpyHostToDevice));
+    ISMG_H2D(spec, S.spec.data(), sizeof(double) * S.spec.size());
     e->D.spec = spec, p += sizeof(double) * S.spec.size();
     e->D.resw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;
     e->D.sumw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;

@@ -656,13 +656,13 @@ Sp2Engine* sp2_try_create(const CoarseOpH& op, int device) {
     const size_t bytes = bufb * size_t(T.B + 2) + sizeof(double) * S.spec.size() + sizeof(unsigned long long) * P +
                          sizeof(unsigned) * T.B + 2 * sizeof(double) * T.B + 64 + 1024;
     ISMG_CUDA(cudaMalloc(&e->mem, bytes));
-    ISMG_CUDA(cudaMemset(e->mem, 0, bytes));
+    ISMG_ZERO(e->mem, bytes);
     char* p = static_cast<char*>(e->mem);
     e->D.bufs = reinterpret_cast<double*>(p), p += bufb * T.B;
     e->D.zero = reinterpret_cast<double*>(p), p += bufb;
     e->D.bd = reinterpret_cast<double*>(p), p += bufb;
     double* spec = reinterpret_cast<double*>(p);
-    ISMG_CUDA(cudaMemcpy(spec, S.spec.data(), sizeof(double) * S.spec.size(), cudaMemcpyHostToDevice));
+    ISMG_H2D(spec, S.spec.data(), sizeof(double) * S.spec.size());
     e->D.spec = spec, p += sizeof(double) * S.spec.size();
     e->D.resw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;
     e->D.sumw = reinterpret_cast<double*>(p), p += sizeof(double) * T.B;

@@ -27,6 +27,25 @@ struct Status : std::runtime_error {
             ::ismgb::fail(ISMG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Zero freshly allocated device memory and wait for it. cudaMemset runs on the
+// legacy default stream, which does NOT order against the context's non-blocking
+// stream: without the wait, a later upload or kernel on that stream could run
+// before the memset and have its data zeroed (seen as a rare solve that read
+// b = 0 and "converged" with residual 0).
+#define ISMG_ZERO(ptr, bytes)                                         \
+    do {                                                              \
+        ISMG_CUDA(cudaMemset((ptr), 0, (bytes)));      \
+        ISMG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));           \
+    } while (0)
+// A blocking host-to-device copy of setup data (tables, weights), complete before
+// anything on a non-blocking stream can read it (a pageable cudaMemcpy may return
+// before its DMA lands).
+#define ISMG_H2D(dst, src, bytes)                                                \
+    do {                                                                         \
+        ISMG_CUDA(cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice));    \
+        ISMG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));                      \
+    } while (0)
+
 // ---------------------------------------------------------------------------
 // Device field layout: the reference's logical ghosted
 // layout embedded in a padded, pitched allocation. Logical (i, j) lives at

@@ -215,7 +215,7 @@ static void plan_coarse(FusedEngine& ee, const CoarseOpH& h, int device) {
     if (!force_rw && allow_cl && cl_coarse_plan(h, e->cl, spec, e->coarse_smem)) {
         e->coarse_kind = 3;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
-        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_H2D(e->tm_spec, spec.data(), sizeof(double) * spec.size());
         ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * cl_backup_doubles(e->cl)));
         size_t smax = e->coarse_smem;
         // hybrid when the grid also fits one SM and the cluster is 2 SMs: a 2048^2
@@ -238,7 +238,7 @@ static void plan_coarse(FusedEngine& ee, const CoarseOpH& h, int device) {
     } else if (allow_tmem && tmem_coarse_plan(h, e->tm, spec, e->coarse_smem)) {
         e->coarse_kind = 2;
         ISMG_CUDA(cudaMalloc(&e->tm_spec, sizeof(double) * spec.size()));
-        ISMG_CUDA(cudaMemcpy(e->tm_spec, spec.data(), sizeof(double) * spec.size(), cudaMemcpyHostToDevice));
+        ISMG_H2D(e->tm_spec, spec.data(), sizeof(double) * spec.size());
         ISMG_CUDA(cudaMalloc(&e->coarse_backup, sizeof(double) * size_t(P.ncy + 2) * e->tm.pitch));
         set_coarse_tmem_smem(e->coarse_smem);
     } else if (allow_smem && size_t(P.ncx + 2) * (P.ncy + 2) * sizeof(double) <= 200 * 1024) {
@@ -347,12 +347,12 @@ FusedEngine* make_fused(Solver& s) {
         const size_t data = sizeof(double) * size_t(2) * size_t(R) * size_t(len);
         const size_t bytes = data + 256;
         ISMG_CUDA(cudaMalloc(&e->xbuf, bytes));
-        ISMG_CUDA(cudaMemset(e->xbuf, 0, bytes));
+        ISMG_ZERO(e->xbuf, bytes);
         ISMG_CUDA(cudaMalloc(&e->bar_scratch, sizeof(double) * 8 * size_t(R)));
         cudaIpcMemHandle_t h;
         ISMG_CUDA(cudaIpcGetMemHandle(&h, e->xbuf));
         static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-        ISMG_CUDA(cudaMemcpy(e->bar_scratch + 8 * rank, &h, 64, cudaMemcpyHostToDevice));
+        ISMG_H2D(e->bar_scratch + 8 * rank, &h, 64);
         std::vector<double> all(size_t(8) * size_t(R));
         double* d_all = nullptr;
         ISMG_CUDA(cudaMalloc(&d_all, sizeof(double) * all.size()));
@@ -416,7 +416,7 @@ FusedEngine* make_fused(Solver& s) {
     const int ngrp = (nb + 31) / 32;
     ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 3 * size_t(nb + ngrp)));
     ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned) * size_t(2 + ngrp)));
-    ISMG_CUDA(cudaMemset(P.ticket, 0, sizeof(unsigned) * size_t(2 + ngrp)));
+    ISMG_ZERO(P.ticket, sizeof(unsigned) * size_t(2 + ngrp));
     P.visit_cap = int(std::min<long long>(P.max_total + 2, 1 << 22));
     ISMG_CUDA(cudaMalloc(&e->d_log, sizeof(int) * 2 * P.visit_cap));
     P.visit_log = e->d_log;

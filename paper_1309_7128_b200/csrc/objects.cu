@@ -13,7 +13,7 @@ void DevBuf::alloc(int w, int h) {
     rows = int64_t(kYOff) + h + kPadTop;
     bytes = size_t(pitch) * size_t(rows) * sizeof(double);
     ISMG_CUDA(cudaMalloc(&base, bytes));
-    ISMG_CUDA(cudaMemset(base, 0, bytes));
+    ISMG_ZERO(base, bytes);
 }
 
 void DevBuf::free() {
@@ -42,9 +42,9 @@ Ctx::Ctx(int dev, cudaStream_t st) : device(dev) {
     }
     ISMG_CUDA(cudaMalloc(&s.part, sizeof(double) * Scratch::kMaxPartials));
     ISMG_CUDA(cudaMalloc(&s.scal, sizeof(double) * Scratch::kScalars));
-    ISMG_CUDA(cudaMemset(s.scal, 0, sizeof(double) * Scratch::kScalars));
+    ISMG_ZERO(s.scal, sizeof(double) * Scratch::kScalars);
     ISMG_CUDA(cudaMalloc(&s.ticket, sizeof(unsigned) * 64));
-    ISMG_CUDA(cudaMemset(s.ticket, 0, sizeof(unsigned) * 64));
+    ISMG_ZERO(s.ticket, sizeof(unsigned) * 64);
     ISMG_CUDA(cudaMallocHost(&s.host, sizeof(double) * Scratch::kScalars));
 }
 

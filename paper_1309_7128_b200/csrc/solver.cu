@@ -22,10 +22,10 @@ static void upload_axis(const TileAxisH& a, AxisDev& d) {
     ISMG_CUDA(cudaMalloc(&d.k1, sizeof(int) * a.n));
     ISMG_CUDA(cudaMalloc(&d.t, sizeof(double) * a.n));
     ISMG_CUDA(cudaMalloc(&d.dk, sizeof(double) * a.n));
-    ISMG_CUDA(cudaMemcpy(d.k0, a.k0.data(), sizeof(int) * a.n, cudaMemcpyHostToDevice));
-    ISMG_CUDA(cudaMemcpy(d.k1, a.k1.data(), sizeof(int) * a.n, cudaMemcpyHostToDevice));
-    ISMG_CUDA(cudaMemcpy(d.t, a.t.data(), sizeof(double) * a.n, cudaMemcpyHostToDevice));
-    ISMG_CUDA(cudaMemcpy(d.dk, a.dk.data(), sizeof(double) * a.n, cudaMemcpyHostToDevice));
+    ISMG_H2D(d.k0, a.k0.data(), sizeof(int) * a.n);
+    ISMG_H2D(d.k1, a.k1.data(), sizeof(int) * a.n);
+    ISMG_H2D(d.t, a.t.data(), sizeof(double) * a.n);
+    ISMG_H2D(d.dk, a.dk.data(), sizeof(double) * a.n);
 }
 
 static void free_axis(AxisDev& d) {
@@ -35,7 +35,7 @@ static void free_axis(AxisDev& d) {
 
 void LevelDev::upload(Ctx& c, int, int) {
     ISMG_CUDA(cudaMalloc(&d_w, sizeof(double) * h.w.size()));
-    ISMG_CUDA(cudaMemcpy(d_w, h.w.data(), sizeof(double) * h.w.size(), cudaMemcpyHostToDevice));
+    ISMG_H2D(d_w, h.w.data(), sizeof(double) * h.w.size());
     upload_axis(h.ax, ax);
     upload_axis(h.ay, ay);
     x = std::make_unique<Field>(&c, h.ncx, h.ncy);

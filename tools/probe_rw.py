@@ -23,3 +23,13 @@ for budget in BUDGETS:
     ms = min(s.bench_coarse_visit(dcb, dce, budget, budget)[2] for _ in range(3))
     print("coarse %d^2 engine %d: %5d sweeps in one group: %8.3f ms  (%.2f us/sweep)"
           % (ncx, s.last_stats()["coarse_engine"], budget, ms, 1e3 * ms / budget), flush=True)
+    if os.environ.get("ISMG_SP_TRACE"):  # a -DISMG_SP_TRACE build: CTA 0's phase clock per visit
+        import ctypes
+        from paper_1309_7128_b200 import _lib
+        tr = (ctypes.c_ulonglong * 6)()
+        _lib.lib().ismg_debug_sp_trace(tr)  # reset, then one more visit
+        s.bench_coarse_visit(dcb, dce, budget, budget)
+        _lib.lib().ismg_debug_sp_trace(tr)
+        v = max(1, tr[5])
+        print("   phases (us per visit): setup %.1f  sweep0 %.1f  rest %.1f  gridsync %.1f  write %.1f  (visits %d)"
+              % tuple([tr[i] / v / 1e3 for i in range(5)] + [tr[5]]), flush=True)
