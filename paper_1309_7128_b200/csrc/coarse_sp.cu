@@ -787,6 +787,7 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     T.singular = op.singular ? 1 : 0;
     T.tend = (op.ncx + kDHiPad + kR - kDLo) + kStride * (nb - 1);
     T.nseg = 8;  // residual chunks per block: 8 segments of the block's ncx + 62 diagonals
+    if (const char* e = getenv("ISMG_SP_NSEG")) T.nseg = std::max(1, std::min(64, atoi(e)));  // tuning hook
     T.seglen = (op.ncx + 62 + T.nseg - 1) / T.nseg;
     const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * kEW + kQB * 32) + S.spec.size());
     ISMG_CUDA(cudaFuncSetAttribute(coarse_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

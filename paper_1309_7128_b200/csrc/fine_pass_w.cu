@@ -926,7 +926,9 @@ int fine_pass_w_quads(int tile) {
 }
 int fine_pass_w_resident(bool mp, int device) {
     int per_sm = 0, sms = 0;
-    if (mp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<true, 0>, 32, 0);
+    // multi-GPU: the sweep-only kernel the passes launch (the all-phases kernel is an A/B hook);
+    // sized on it, 4 GPUs at 16384^2 take 64-row chunks: 226.9 G against 222.1 G with 96
+    if (mp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<true, 1>, 32, 0);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fine_pass_w_kernel<false, 0>, 32, 0);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return std::max(1, per_sm) * std::max(1, sms);
