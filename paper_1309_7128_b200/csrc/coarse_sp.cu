@@ -36,6 +36,8 @@
 #include <cstring>
 #include <vector>
 
+#include <type_traits>
+
 #include "fused_impl.cuh"
 
 namespace ismgb {
@@ -135,6 +137,21 @@ extern __shared__ __align__(16) double sp_dyn[];
 
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+// shared-memory loads / stores by 32-bit address (the rings: no generic-to-shared
+// conversion and no 64-bit address arithmetic per step)
+__device__ __forceinline__ double lds64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 lds128(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -259,6 +276,7 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     double* rE = ringE + size_t(b) * kQE * kEW + lane;
     double* rB = ringB + size_t(b) * kQB * 32 + lane;
     const uint32_t sE = su32(rE), sB = su32(rB);
+    const uint32_t sN = su32(rN) + 8u * uint32_t(lane), sT = su32(tbl);  // this lane's ring column, class table
     const bool has_n = b + 1 < T.nb, has_p = b > 0;
     const double* xo_b = xo + size_t(b) * T.bstride + lane;
     const double* xo_n = (has_n ? xo + size_t(b + 1) * T.bstride : D.zero);  // row 32 (b+1) = next block's lane 0
@@ -301,116 +319,123 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
         const double* pB = bd_b + o0 + size_t(kK) * 32;
         const double* pX = xo_n + o0 + size_t(kK) * 32 - 61 * 32;        // lane 31: row 32, column I + 1
         double* pO = xn_b + o0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int t = 8 * m + j;
-            auto nslot = [&](int q) {  // ring offset of CTA step 8m + q (q folds to a constant)
-                const int seg = q >> 3;
-                return (seg == 0 ? sBn : (seg == -1 ? sA : sC)) + (q & 7) * kRows;
-            };
-            auto bslot = [&](int q) { return (((q >> 3) & 1) ? b1 : b0) + (q & 7) * 32; };
-            if ((j & 3) == 0 && avail < min(t + 3 + kK + kD + 4, T.tend + 1)) {  // sweep g-1 far enough
-                const int need = min(t + 3 + kK + kD + 4, T.tend + 1);  // (its last step: no wait for its fold)
-                if (lane == 0) {
-                    const long long tw = gtimer();
-                    int a;
-                    while ((a = ld_acq_cta(&sh.avail)) < need) {
-                        if (ld_vol_s(&sh.abort_) || timed_out(tw)) break;
+        // a group whose 8 steps all prefetch and update (the common case) runs without the
+        // per-step window tests, so the history registers rotate without copies
+        auto group = [&](auto fullc) {
+            constexpr bool FULL = decltype(fullc)::value;
+    #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int t = 8 * m + j;
+                auto nslot = [&](int q) {  // ring offset of CTA step 8m + q (q folds to a constant)
+                    const int seg = q >> 3;
+                    return (seg == 0 ? sBn : (seg == -1 ? sA : sC)) + (q & 7) * kRows;
+                };
+                auto bslot = [&](int q) { return (((q >> 3) & 1) ? b1 : b0) + (q & 7) * 32; };
+                if ((j & 3) == 0 && avail < min(t + 3 + kK + kD + 4, T.tend + 1)) {  // sweep g-1 far enough
+                    const int need = min(t + 3 + kK + kD + 4, T.tend + 1);  // (its last step: no wait for its fold)
+                    if (lane == 0) {
+                        const long long tw = gtimer();
+                        int a;
+                        while ((a = ld_acq_cta(&sh.avail)) < need) {
+                            if (ld_vol_s(&sh.abort_) || timed_out(tw)) break;
+                        }
+                        avail = a;
                     }
-                    avail = a;
+                    avail = __shfl_sync(kFull, avail, 0);
+                    __syncwarp();
                 }
-                avail = __shfl_sync(kFull, avail, 0);
+                const int d = d0 + j;
+    #ifndef ISMG_SPX_NOCP
+                if (FULL || (d + kK >= kDLo && d + kK <= dhi + kR)) {  // prefetch for step t + kK
+                    SP_ASSERT(d + kK - 61 + kDOff >= 0 && d + kK + 1 + kDOff < T.dspan, "prefetch diagonal");
+                    SP_ASSERT(bslot(j + kK) >= 0 && bslot(j + kK) < kQB * 32, "rhs ring slot");
+                    cp8(sE + 8u * uint32_t(((j + kK) & 7) * kEW), pE + 32 * j);
+                    cp8(sB + 8u * uint32_t(bslot(j + kK)), pB + 32 * j);
+                    // lane 31: row 32 into position 32 of the slot its NE read of step t + kK uses
+                    if (lane == 31) cp8(sE + 8u * uint32_t(((j + kK + 2) & 7) * kEW + 1), pX + 32 * j);
+                }
+    #endif
+                cp_commit();
+                cp_wait<kK - 2>();
                 __syncwarp();
+                if (FULL || (d >= kDLo && d <= dhi + kR)) {
+                    // ---- update of column I (sweep g) ----
+                    const int I = d - 2 * lane;
+                    const bool act_u = rowok && unsigned(I) < unsigned(ncx) && d <= dhi;
+                    SP_ASSERT(nslot(j - kR - 1) >= 0 && nslot(j + kD) + kRows <= kQ * kRows, "new-value ring slot");
+                    SP_ASSERT(bslot(j - kR) >= 0 && bslot(j) < kQB * 32, "rhs ring slot");
+                    SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
+                    SP_ASSERT(!has_n || b + 1 < T.nb, "mirror target");
+                    const double E = lds64(sE + 8u * uint32_t((j & 7) * kEW));
+                    const double NE = lds64(sE + 8u * uint32_t(((j + 2) & 7) * kEW + 1));  // lane 31: position 32
+                    const double SE = lds64(sN + 8u * uint32_t(nslot(j - 1)));
+                    const double bu = lds64(sB + 8u * uint32_t(bslot(j)));
+                    const uint32_t wu = sT + 80u * uint32_t(I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls));
+                    const double2 u01 = lds128(wu), u23 = lds128(wu + 16), u45 = lds128(wu + 32), u67 = lds128(wu + 48),
+                                  u89 = lds128(wu + 64);
+                    double acc = 0.0;
+                    acc += u01.y * E;
+                    acc += u23.x * outP;
+                    acc += u23.y * neP;
+                    acc += u45.x * seP;
+                    acc += u45.y * NE;
+                    acc += u67.x * neP2;
+                    acc += u67.y * SE;
+                    acc += u89.x * seP2;
+                    const double num = act_u ? bu - acc : 1.0;
+                    const double q = div_full(num, u01.x, u89.y);
+                    const double out = act_u ? q : 0.0;
+                    sts64(sN + 8u * uint32_t(nslot(j) + 1), out);
+                    if (lane == 31 && has_n) sts64(sN + 8u * uint32_t(kQ * kRows + nslot(j + kD) - 31), out);  // row -1 of the next block
+    #ifdef ISMG_SP_INLINE_RES
+                    if (lane == 0 && has_p) rN[nslot(j - kD) + 33 - kQ * kRows] = out;  // row 32 of the previous block
+    #endif
+    #ifndef ISMG_SPX_NOSTG
+                    if (d <= dhi) pO[32 * j] = out;
+    #endif
+                    if (act_u) rsum += out;
+                    seP2 = seP, seP = SE, neP2 = neP, neP = NE, outP = out;
+    #ifdef ISMG_SP_INLINE_RES
+                    // ---- residual of column I - kR (sweep g values on all nine points) ----
+                    const int Ir = I - kR;
+                    const bool act_r = rowok && unsigned(Ir) < unsigned(ncx);
+                    qSW = qS, qS = qSE, qSE = rN[nslot(j - kR - 1) + lane];
+                    qW = qC, qC = qE, qE = rN[nslot(j - kR + 1) + lane + 1];
+                    qNW = qN, qN = qNE, qNE = rN[nslot(j - kR + 3) + lane + 2];
+                    const double br = rB[bslot(j - kR)];
+                    const double2* wr = reinterpret_cast<const double2*>(
+                        tbl + 10 * (Ir == 0 ? wcls : (Ir == ncx - 1 ? ecls : bcls)));
+                    const double2 r01 = wr[0], r23 = wr[1], r45 = wr[2], r67 = wr[3], r89 = wr[4];
+                    double a = r01.x * qC;
+                    a += r01.y * qE;
+                    a += r23.x * qW;
+                    a += r23.y * qN;
+                    a += r45.x * qS;
+                    a += r45.y * qNE;
+                    a += r67.x * qNW;
+                    a += r67.y * qSE;
+                    a += r89.x * qSW;
+                    double mm = act_r ? fabs(br - a) : 0.0;
+                    mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
+                    lmax = fmax(lmax, mm);
+    #endif
+                }
+    #ifdef ISMG_SPX_NOBAR
+                if (false) {
+    #else
+                if ((j % kS) == kS - 1) {
+    #endif  // named barrier of the compute warps every kS steps
+                    if (b == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
+                    bar_compute(nthr);
+                    if (b == 0 && lane == 0) st_rel_cta(&sh.done_t, max(0, t + 1));
+                    aborted = ld_vol_s(&sh.dec[h & 1]) != 0;
+                    ++h;
+                    if (aborted) break;
+                }
             }
-            const int d = d0 + j;
-#ifndef ISMG_SPX_NOCP
-            if (d + kK >= kDLo && d + kK <= dhi + kR) {  // prefetch for step t + kK
-                SP_ASSERT(d + kK - 61 + kDOff >= 0 && d + kK + 1 + kDOff < T.dspan, "prefetch diagonal");
-                SP_ASSERT(bslot(j + kK) >= 0 && bslot(j + kK) < kQB * 32, "rhs ring slot");
-                cp8(sE + 8u * uint32_t(((j + kK) & 7) * kEW), pE + 32 * j);
-                cp8(sB + 8u * uint32_t(bslot(j + kK)), pB + 32 * j);
-                // lane 31: row 32 into position 32 of the slot its NE read of step t + kK uses
-                if (lane == 31) cp8(sE + 8u * uint32_t(((j + kK + 2) & 7) * kEW + 1), pX + 32 * j);
-            }
-#endif
-            cp_commit();
-            cp_wait<kK - 2>();
-            __syncwarp();
-            if (d >= kDLo && d <= dhi + kR) {
-                // ---- update of column I (sweep g) ----
-                const int I = d - 2 * lane;
-                const bool act_u = rowok && unsigned(I) < unsigned(ncx) && d <= dhi;
-                SP_ASSERT(nslot(j - kR - 1) >= 0 && nslot(j + kD) + kRows <= kQ * kRows, "new-value ring slot");
-                SP_ASSERT(bslot(j - kR) >= 0 && bslot(j) < kQB * 32, "rhs ring slot");
-                SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
-                SP_ASSERT(!has_n || b + 1 < T.nb, "mirror target");
-                const double E = rE[(j & 7) * kEW];
-                const double NE = rE[((j + 2) & 7) * kEW + 1];  // lane 31: position 32
-                const double SE = rN[nslot(j - 1) + lane];
-                const double bu = rB[bslot(j)];
-                const double2* wu = reinterpret_cast<const double2*>(
-                    tbl + 10 * (I == 0 ? wcls : (I == ncx - 1 ? ecls : bcls)));
-                const double2 u01 = wu[0], u23 = wu[1], u45 = wu[2], u67 = wu[3], u89 = wu[4];
-                double acc = 0.0;
-                acc += u01.y * E;
-                acc += u23.x * outP;
-                acc += u23.y * neP;
-                acc += u45.x * seP;
-                acc += u45.y * NE;
-                acc += u67.x * neP2;
-                acc += u67.y * SE;
-                acc += u89.x * seP2;
-                const double num = act_u ? bu - acc : 1.0;
-                const double q = div_full(num, u01.x, u89.y);
-                const double out = act_u ? q : 0.0;
-                rN[nslot(j) + lane + 1] = out;
-                if (lane == 31 && has_n) rN[kQ * kRows + nslot(j + kD)] = out;      // row -1 of the next block
-#ifdef ISMG_SP_INLINE_RES
-                if (lane == 0 && has_p) rN[nslot(j - kD) + 33 - kQ * kRows] = out;  // row 32 of the previous block
-#endif
-#ifndef ISMG_SPX_NOSTG
-                if (d <= dhi) pO[32 * j] = out;
-#endif
-                if (act_u) rsum += out;
-                seP2 = seP, seP = SE, neP2 = neP, neP = NE, outP = out;
-#ifdef ISMG_SP_INLINE_RES
-                // ---- residual of column I - kR (sweep g values on all nine points) ----
-                const int Ir = I - kR;
-                const bool act_r = rowok && unsigned(Ir) < unsigned(ncx);
-                qSW = qS, qS = qSE, qSE = rN[nslot(j - kR - 1) + lane];
-                qW = qC, qC = qE, qE = rN[nslot(j - kR + 1) + lane + 1];
-                qNW = qN, qN = qNE, qNE = rN[nslot(j - kR + 3) + lane + 2];
-                const double br = rB[bslot(j - kR)];
-                const double2* wr = reinterpret_cast<const double2*>(
-                    tbl + 10 * (Ir == 0 ? wcls : (Ir == ncx - 1 ? ecls : bcls)));
-                const double2 r01 = wr[0], r23 = wr[1], r45 = wr[2], r67 = wr[3], r89 = wr[4];
-                double a = r01.x * qC;
-                a += r01.y * qE;
-                a += r23.x * qW;
-                a += r23.y * qN;
-                a += r45.x * qS;
-                a += r45.y * qNE;
-                a += r67.x * qNW;
-                a += r67.y * qSE;
-                a += r89.x * qSW;
-                double mm = act_r ? fabs(br - a) : 0.0;
-                mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
-                lmax = fmax(lmax, mm);
-#endif
-            }
-#ifdef ISMG_SPX_NOBAR
-            if (false) {
-#else
-            if ((j % kS) == kS - 1) {
-#endif  // named barrier of the compute warps every kS steps
-                if (b == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
-                bar_compute(nthr);
-                if (b == 0 && lane == 0) st_rel_cta(&sh.done_t, max(0, t + 1));
-                aborted = ld_vol_s(&sh.dec[h & 1]) != 0;
-                ++h;
-                if (aborted) break;
-            }
-        }
+        };
+        if (d0 >= kDLo && d0 + 7 + kK <= dhi + kR) group(std::true_type{});
+        else group(std::false_type{});
     }
     cp_wait<0>();
 #ifndef ISMG_SP_INLINE_RES
