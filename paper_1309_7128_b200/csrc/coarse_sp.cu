@@ -811,7 +811,10 @@ SpEngine* sp_try_create(const CoarseOpH& op, int device) {
     T.spec_words = int(S.spec.size());
     T.singular = op.singular ? 1 : 0;
     T.tend = (op.ncx + kDHiPad + kR - kDLo) + kStride * (nb - 1);
-    T.nseg = 8;  // residual chunks per block: 8 segments of the block's ncx + 62 diagonals
+    // residual chunks per block: 16 segments of the block's ncx + 62 diagonals. Same-box A/B
+    // (tools/visit_hist.py 16384 32 3, coarse ms of steps 1-3): 16 -> 387 / 211 / 247,
+    // 8 -> 406 / 236 / 285, 32 -> 430 / 241 / 286 (profiles/r02_ab_sp_nseg.txt)
+    T.nseg = 16;
     if (const char* e = getenv("ISMG_SP_NSEG")) T.nseg = std::max(1, std::min(64, atoi(e)));  // tuning hook
     T.seglen = (op.ncx + 62 + T.nseg - 1) / T.nseg;
     const size_t smem = sizeof(double) * (size_t(nb) * (kQ * kRows + kQE * kEW + kQB * 32) + S.spec.size());
