@@ -12,6 +12,8 @@
 #include <cstring>
 #include <vector>
 
+#include <type_traits>
+
 #include "fused_impl.cuh"
 
 namespace ismgb {
@@ -392,6 +394,19 @@ __device__ __forceinline__ void sp_sweep(const Sp2K& T, const Sp2D& D, Sp2Shared
         }
         const bool live = b < T.nb;
         const bool pf_any = live && d0 + 3 + kK >= kDLo - kR && d0 + kK <= dhi + kR;
+#ifndef ISMG_SP_NOIDLE
+        if (!pf_any && !(live && d0 + 3 >= kDLo && d0 <= dhi + kR)) {  // an idle group: the barrier only
+            if (w == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
+            bar_compute(nthr);
+            if (w == 0 && lane == 0) st_rel_cta(&sh.done_t, max(0, 4 * m + 4));
+            aborted = ld_vol_s(&sh.dec[h & 1]) != 0;
+            ++h;
+            continue;
+        }
+#endif
+        // a group whose 4 steps all prefetch and update runs without the per-step window tests
+        auto group = [&](auto fullc) {
+            constexpr bool FULL = decltype(fullc)::value;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int t = 4 * m + j;
@@ -409,12 +424,13 @@ __device__ __forceinline__ void sp_sweep(const Sp2K& T, const Sp2D& D, Sp2Shared
                 avail = __shfl_sync(kFull, avail, 0);
                 __syncwarp();
             }
-            if (live && d + kK >= kDLo - kR && d + kK <= dhi + kR)
+            if (FULL || (live && d + kK >= kDLo - kR && d + kK <= dhi + kR))
                 blk_prefetch(w, eslot(j + kK), d + kK, M, xo_row, xo_next, bd_row);
             cp_commit();
             cp_wait<kK - 2>();
             __syncwarp();
-            if (live && d >= kDLo && d <= dhi + kR) blk_step(B, w, b, rowok, j, d, T, M, dn, dp, xn_row, nslot, eslot);
+            if (FULL || (live && d >= kDLo && d <= dhi + kR))
+                blk_step(B, w, b, rowok, j, d, T, M, dn, dp, xn_row, nslot, eslot);
             if (j == 3) {  // named barrier of the compute warps every kS = 4 steps
                 if (w == 0 && lane == 0) sh.dec[h & 1] = ld_vol_s(&sh.abort_);
                 bar_compute(nthr);
@@ -423,6 +439,12 @@ __device__ __forceinline__ void sp_sweep(const Sp2K& T, const Sp2D& D, Sp2Shared
                 ++h;
             }
         }
+        };
+#ifndef ISMG_SP2_NOFULL
+        if (live && d0 >= kDLo && d0 + 3 + kK <= dhi + kR) group(std::true_type{});
+        else
+#endif
+            group(std::false_type{});
     }
     cp_wait<0>();
     if (b < T.nb) {  // the last block's sum
