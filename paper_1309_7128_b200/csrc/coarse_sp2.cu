@@ -100,6 +100,15 @@ extern __shared__ __align__(16) double sp2_dyn[];
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
+// shared-memory loads / stores by 32-bit address
+__device__ __forceinline__ double lds64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -239,20 +248,22 @@ __device__ __forceinline__ void blk_step(Blk& B, int w, int b, bool rowok, int j
     const bool act_u = rowok && unsigned(I) < unsigned(ncx) && d <= dhi;
     const bool act_r = rowok && unsigned(Ir) < unsigned(ncx);
     const double* tbl = sp2_dyn + M.tbl;
-    double* rN = sp2_dyn + w * (kQ * kRows);
-    const double* rE = sp2_dyn + M.e + w * (kQE * 32) + lane;
-    const double* rB = sp2_dyn + M.bu + w * (2 * kQB * 32) + lane;
+    const uint32_t s0 = su32(sp2_dyn);
+    const uint32_t sN = s0 + 8u * uint32_t(w * (kQ * kRows) + lane);  // this lane's column of the warp's ring
+    const uint32_t sE = s0 + 8u * uint32_t(M.e + w * (kQE * 32) + lane);
+    const uint32_t sB = s0 + 8u * uint32_t(M.bu + w * (2 * kQB * 32) + lane);
     SP_ASSERT(nslot(j - kR - 1) >= 0 && nslot(j + kD) + kRows <= kQ * kRows, "new-value ring slot");
     SP_ASSERT(d + kDOff >= 0 && d + kDOff < T.dspan, "output diagonal");
     // inputs of both cells (none is written by this step)
-    const double E = rE[eslot(j) * 32];
-    const double NE = lane < 31 ? rE[eslot(j + 2) * 32 + 1] : sp2_dyn[M.x + w * kQE + eslot(j)];
-    const double SE = rN[nslot(j - 1) + lane];
-    const double bu = rB[eslot(j) * 32];
-    const double rm1 = rN[nslot(j - kR - 1) + lane];
-    const double r0 = rN[nslot(j - kR + 1) + lane + 1];
-    const double rp1 = rN[nslot(j - kR + 3) + lane + 2];
-    const double br = rB[kQB * 32 + eslot(j) * 32];
+    const double E = lds64(sE + 8u * uint32_t(eslot(j) * 32));
+    const double NE = lds64(lane < 31 ? sE + 8u * uint32_t(eslot(j + 2) * 32 + 1)
+                                      : s0 + 8u * uint32_t(M.x + w * kQE + eslot(j)));
+    const double SE = lds64(sN + 8u * uint32_t(nslot(j - 1)));
+    const double bu = lds64(sB + 8u * uint32_t(eslot(j) * 32));
+    const double rm1 = lds64(sN + 8u * uint32_t(nslot(j - kR - 1)));
+    const double r0 = lds64(sN + 8u * uint32_t(nslot(j - kR + 1) + 1));
+    const double rp1 = lds64(sN + 8u * uint32_t(nslot(j - kR + 3) + 2));
+    const double br = lds64(sB + 8u * uint32_t(kQB * 32 + eslot(j) * 32));
     B.qSW = B.qS, B.qS = B.qSE, B.qSE = rm1;
     B.qW = B.qC, B.qC = B.qE, B.qE = r0;
     B.qNW = B.qN, B.qN = B.qNE, B.qNE = rp1;
@@ -294,9 +305,9 @@ __device__ __forceinline__ void blk_step(Blk& B, int w, int b, bool rowok, int j
     mm = (mm != mm) ? 0.0 : mm;  // std::max drops NaN
     B.lmax = fmax(B.lmax, mm);
     // ---- stores: own row, the neighbour blocks' mirror rows, the sweep's output ----
-    rN[nslot(j) + lane + 1] = out;
-    if (lane == 31 && b + 1 < T.nb) rN[dn + nslot(j + kD)] = out;  // row -1 of block b+1 (next warp's ring)
-    if (lane == 0 && b > 0) rN[dp + nslot(j - kD) + 33] = out;     // row 32 of block b-1 (previous warp's ring)
+    sts64(sN + 8u * uint32_t(nslot(j) + 1), out);
+    if (lane == 31 && b + 1 < T.nb) sts64(sN + 8u * uint32_t(dn + nslot(j + kD) - 31), out);  // row -1 of block b+1 (next warp's ring)
+    if (lane == 0 && b > 0) sts64(sN + 8u * uint32_t(dp + nslot(j - kD) + 33), out);          // row 32 of block b-1 (previous warp's ring)
 #ifndef ISMG_SPX_NOSTG
     if (d <= dhi) xn_row[(d + kDOff) * 32] = out;
 #endif
