@@ -885,6 +885,334 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     warp_epilogue<MP>(P, prolong ? kProlong : kResid, A.mx, A.sx, A.cm, A.nan, st);
 }
 
+// ---- FUSED (kFused; single GPU, uniform power-of-two tiles): the prolongation pass
+// and the first sweep after it in ONE HBM pass. Row k is loaded and prolonged,
+// x' = (x + c) + P ce (coarsening.hpp:495-500; the fast rows of prolong_w2), then
+// shifted by the prolonged field's anchor, x'' = x' + c' (cycles.hpp:142; c' from
+// prolong_sum_kernel as -(sum of P ce) / cells, the field being anchored before).
+// The prolongation's residual rp (cycles.hpp:141) is formed on the unrelaxed rows
+// k-2 (a pristine copy), k-1, k; then the red / black sweep, its residual and tile
+// sums run exactly as in sweep_w (cycles.hpp:148-152). The pass reads x, b and
+// writes x once: the two passes it replaces moved 48 B per cell, it moves 24.
+#ifndef ISMG_FINE_MINB_FU
+#define ISMG_FINE_MINB_FU 12
+#endif
+constexpr int kFuRows = 104;  // staged y-axis rows: chunk + 3 + 3 halo + 1
+
+struct ProW {
+    double ar[4], sr[4];  // column weights (dx - s) / dx, s / dx (exact: dx is a power of two)
+    int i0, i1;           // the quad's coarse pair (one per quad on uniform tiles)
+};
+
+template <int U, int P1>
+__device__ __forceinline__ void step_f(const SmemW& sm, int slot, const Lane& L, const Geo& G, Win& w, Acc& A, int k,
+                                       const ProW& pw, double cN, double ca, double cb, double* px, double& mxp) {
+    constexpr int s0 = U, s1 = (U + 3) & 3, s2 = (U + 2) & 3, s3 = (U + 1) & 3;
+    const int si = 4 * L.l;
+    double t[4];
+    {
+        const double2 v01 = *reinterpret_cast<const double2*>(&sm.x[slot][si]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&sm.x[slot][si + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&sm.b[slot][si]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&sm.b[slot][si + 2]);
+        const double raw[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = ((raw[q] + G.c) + (pw.ar[q] * ca + pw.sr[q] * cb)) + cN;
+        if (k < 0 || k >= G.ny || L.frozen) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[q] = 0.0;
+        } else if (L.spec) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[q] = L.dom[q] ? t[q] : 0.0;
+        }
+        w.b[s0][0] = b01.x, w.b[s0][1] = b01.y, w.b[s0][2] = b23.x, w.b[s0][3] = b23.y;
+    }
+    double* x1 = w.x[s1];
+    double* x2 = w.x[s2];
+    double* x3 = w.x[s3];
+    const double* x4 = w.x[s0];  // row k-4
+    const double redW = sh_up(x1[3]), redE = sh_dn(x1[0]);  // row k-1, unrelaxed
+    const double blkW = sh_up(x2[3]), blkE = sh_dn(x2[0]);
+    const double resW = sh_up(x3[3]), resE = sh_dn(x3[0]);
+    // ---- rp: residual of the prolonged row j = k-1 (S = row k-2 before its red cells moved)
+    {
+        const int j = k - 1;
+        if (j >= G.r0 && j < G.r1 && L.owned) {
+            const double* b = w.b[s1];
+            double r[4];
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                r[0] = b[0] - ((((redW + x1[1]) + px[0]) + t[0]) - (L.dc[0] + dr) * x1[0]);
+                r[1] = b[1] - ((((x1[0] + x1[2]) + px[1]) + t[1]) - (L.dc[1] + dr) * x1[1]);
+                r[2] = b[2] - ((((x1[1] + x1[3]) + px[2]) + t[2]) - (L.dc[2] + dr) * x1[2]);
+                r[3] = b[3] - ((((x1[2] + redE) + px[3]) + t[3]) - (L.dc[3] + dr) * x1[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            } else {
+                r[0] = b[0] - ((((redW + x1[1]) + px[0]) + t[0]) - 4.0 * x1[0]);
+                r[1] = b[1] - ((((x1[0] + x1[2]) + px[1]) + t[1]) - 4.0 * x1[1]);
+                r[2] = b[2] - ((((x1[1] + x1[3]) + px[2]) + t[2]) - 4.0 * x1[2]);
+                r[3] = b[3] - ((((x1[2] + redE) + px[3]) + t[3]) - 4.0 * x1[3]);
+            }
+            const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
+            mxp = max_drop_nan(mxp, max_drop_nan(m01, m23));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) px[q] = x1[q];  // row k-1 unrelaxed, the next iteration's S
+    // ---- red half-sweep of row j = k-1 (as step_w)
+    {
+        const int j = k - 1;
+        if (j >= G.r0 - 2 && j >= 0 && j < G.ny) {
+            const double* b = w.b[s1];
+            constexpr int qa = P1, qb = qa + 2;
+            const double Wa = qa == 0 ? redW : x1[0], Ea = x1[qa + 1];
+            const double Wb = x1[qb - 1], Eb = qb == 3 ? redE : x1[3];
+            double va = ((((Wa + Ea) + x2[qa]) + t[qa]) - b[qa]) * 0.25;
+            double vb = ((((Wb + Eb) + x2[qb]) + t[qb]) - b[qb]) * 0.25;
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                va = L.red[qa] ? gs_exact(Wa, Ea, x2[qa], t[qa], b[qa], L.dc[qa] + dr) : x1[qa];
+                vb = L.red[qb] ? gs_exact(Wb, Eb, x2[qb], t[qb], b[qb], L.dc[qb] + dr) : x1[qb];
+            }
+            if (!L.frozen) x1[qa] = va, x1[qb] = vb;
+        }
+    }
+    // ---- black half-sweep of row j = k-2
+    {
+        const int j = k - 2;
+        if (j >= G.r0 - 1 && j >= 0 && j < G.ny) {
+            const double* b = w.b[s2];
+            constexpr int qa = P1, qb = qa + 2;
+            const double Wa = qa == 0 ? blkW : x2[0], Ea = x2[qa + 1];
+            const double Wb = x2[qb - 1], Eb = qb == 3 ? blkE : x2[3];
+            double va = ((((Wa + Ea) + x3[qa]) + x1[qa]) - b[qa]) * 0.25;
+            double vb = ((((Wb + Eb) + x3[qb]) + x1[qb]) - b[qb]) * 0.25;
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                va = L.blk[qa] ? gs_exact(Wa, Ea, x3[qa], x1[qa], b[qa], L.dc[qa] + dr) : x2[qa];
+                vb = L.blk[qb] ? gs_exact(Wb, Eb, x3[qb], x1[qb], b[qb], L.dc[qb] + dr) : x2[qb];
+            }
+            if (!L.frozen) x2[qa] = va, x2[qb] = vb;
+        }
+    }
+    // ---- residual of row j = k-3 and store (as step_w)
+    {
+        const int j = k - 3;
+        if (j >= G.r0 && j < G.r1 && L.owned) {
+            const double* b = w.b[s3];
+            double r[4];
+            if ((j == 0) || (j == G.ny - 1) || L.spec) {
+                const double dr = row_part(G, j);
+                r[0] = b[0] - ((((resW + x3[1]) + x4[0]) + x2[0]) - (L.dc[0] + dr) * x3[0]);
+                r[1] = b[1] - ((((x3[0] + x3[2]) + x4[1]) + x2[1]) - (L.dc[1] + dr) * x3[1]);
+                r[2] = b[2] - ((((x3[1] + x3[3]) + x4[2]) + x2[2]) - (L.dc[2] + dr) * x3[2]);
+                r[3] = b[3] - ((((x3[2] + resE) + x4[3]) + x2[3]) - (L.dc[3] + dr) * x3[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) r[q] = L.dom[q] ? r[q] : 0.0;
+            } else {
+                r[0] = b[0] - ((((resW + x3[1]) + x4[0]) + x2[0]) - 4.0 * x3[0]);
+                r[1] = b[1] - ((((x3[0] + x3[2]) + x4[1]) + x2[1]) - 4.0 * x3[1]);
+                r[2] = b[2] - ((((x3[1] + x3[3]) + x4[2]) + x2[2]) - 4.0 * x3[2]);
+                r[3] = b[3] - ((((x3[2] + resE) + x4[3]) + x2[3]) - 4.0 * x3[3]);
+            }
+            const double m01 = max_drop_nan(fabs(r[0]), fabs(r[1])), m23 = max_drop_nan(fabs(r[2]), fabs(r[3]));
+            A.mx = max_drop_nan(A.mx, max_drop_nan(m01, m23));
+            A.sx = A.sx + ((x3[0] + x3[1]) + (x3[2] + x3[3]));
+            A.tacc = A.tacc + ((r[0] + r[1]) + (r[2] + r[3]));
+            put_row(G, L, j, x3);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w.x[s0][q] = t[q];
+}
+
+// the fused pass's epilogue: warp_epilogue<false> with a fourth partial (max |rp|)
+__device__ __forceinline__ void fused_epilogue(const Params& P, double mx, double sx, double cm, int nan,
+                                               double mp) {
+    const int nb = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int ng = (nb + 31) >> 5, grp = bid >> 5;
+    double* gpart = P.part + 4 * nb;
+    mx = warp_max(mx);
+    sx = warp_sum_down(sx);
+    cm = warp_max(cm);
+    mp = warp_max(mp);
+    const int anynan = __any_sync(kFull, nan);
+    unsigned last = 0;
+    if (lane == 0) {
+        P.part[4 * bid] = mx, P.part[4 * bid + 1] = sx, P.part[4 * bid + 2] = cm, P.part[4 * bid + 3] = mp;
+        if (anynan) P.ctl->nan_seen = 1;
+        const unsigned gsize = unsigned(min(32, nb - 32 * grp));
+        last = atom_add_release(&P.ticket[1 + grp], 1u) == gsize - 1;
+    }
+    if (!__shfl_sync(kFull, last, 0)) return;
+    __threadfence();
+    {
+        const int k = 32 * grp + lane;
+        double m = 0.0, s = 0.0, c = 0.0, p = 0.0;
+        if (k < nb)
+            m = __ldcg(&P.part[4 * k]), s = __ldcg(&P.part[4 * k + 1]), c = __ldcg(&P.part[4 * k + 2]),
+            p = __ldcg(&P.part[4 * k + 3]);
+        m = warp_max(m);
+        s = warp_sum_down(s);
+        c = warp_max(c);
+        p = warp_max(p);
+        last = 0;
+        if (lane == 0) {
+            gpart[4 * grp] = m, gpart[4 * grp + 1] = s, gpart[4 * grp + 2] = c, gpart[4 * grp + 3] = p;
+            P.ticket[1 + grp] = 0u;
+            __threadfence();
+            last = atomicAdd(P.ticket, 1u) == unsigned(ng - 1);
+        }
+    }
+    if (!__shfl_sync(kFull, last, 0)) return;
+    __threadfence();
+    double m = 0.0, s = 0.0, c = 0.0, p = 0.0;
+    for (int k = lane; k < ng; k += 32) {
+        m = fmax(m, __ldcg(&gpart[4 * k]));
+        s += __ldcg(&gpart[4 * k + 1]);
+        c = fmax(c, __ldcg(&gpart[4 * k + 2]));
+        p = fmax(p, __ldcg(&gpart[4 * k + 3]));
+    }
+    m = warp_max(m);
+    s = warp_sum_down(s);
+    c = warp_max(c);
+    p = warp_max(p);
+    if (lane == 0) {
+        fine_decide_fused(P, p, m, s, c);
+        publish_phase(P, P.ctl->phase);
+        *P.ticket = 0u;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& st, int nq) {
+    const int W = 4 * nq;
+    const int a = blockIdx.x * W;
+    const Lane L(P, a, nq);
+    Geo G;
+    G.r0 = P.row0 + blockIdx.y * P.H, G.r1 = min(G.r0 + P.H, P.row1), G.ny = P.ny;
+    G.c = st.has_shift ? st.shift : -0.0;
+    G.fwS = face_weight(P.bc.k[ISMG_SIDE_SOUTH]), G.fwN = face_weight(P.bc.k[ISMG_SIDE_NORTH]);
+    G.outp = st.buf[st.cur ^ 1] + L.c0;
+    G.pitch = P.pitch;
+    const double cN = st.fshift;
+    const int tmask = P.tile - 1, lg = ilog2(P.tile);
+    const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
+    const double* xin = st.buf[st.cur];
+    const double* brow0 = st.b + (a - 4);
+    const int kfirst = G.r0 - 3, klast = G.r1 + 2;
+    // the lane's column weights and coarse pair (TileAxis::locate_cell of its columns)
+    ProW pw;
+    pw.i0 = pw.i1 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        pw.ar[q] = pw.sr[q] = 0.0;
+        if (L.dom[q]) {
+            const int col = L.c0 + q;
+            const double sq = P.ax.t[col], dxq = P.ax.dk[col], idx = pow2_recip(dxq);
+            pw.ar[q] = (dxq - sq) * idx, pw.sr[q] = sq * idx;
+            if (q == 0) pw.i0 = P.ax.k0[col], pw.i1 = P.ax.k1[col];
+        }
+    }
+    // the chunk's rows of the y-axis tables, scaled: (dy - t) / dy, t / dy
+    __shared__ double s_w0[kFuRows], s_tt[kFuRows];
+    __shared__ int s_j0[kFuRows], s_j1[kFuRows];
+    for (int i = int(threadIdx.x & 31); i < klast - kfirst + 1; i += 32) {
+        const int k = kfirst + i;
+        const bool in = k >= 0 && k < G.ny;
+        const double t = in ? P.ay.t[k] : 0.0, dk = in ? P.ay.dk[k] : 1.0, idk = pow2_recip(dk);
+        s_w0[i] = (dk - t) * idk, s_tt[i] = t * idk;
+        s_j0[i] = in ? P.ay.k0[k] : 0, s_j1[i] = in ? P.ay.k1[k] : 0;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < kRingW; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
+        issue_row_w(sm, xin + int64_t(kfirst + s) * G.pitch + (a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s,
+                    bytes);
+    Win w;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w.x[s][q] = w.b[s][q] = 0.0;
+    Acc A;
+    double px[4] = {0.0, 0.0, 0.0, 0.0}, mxp = 0.0;
+    int cJ0 = -1, cJ1 = -1;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    const uint32_t bar0 = su32(&sm.bar[0]);
+    int slot = 0;
+    uint32_t phase = 0;
+    auto row = [&](auto u, int k) {
+        constexpr int U = decltype(u)::value;
+        const int i = k - kfirst;
+        const double w0 = s_w0[i], tt = s_tt[i];
+        const int J0 = s_j0[i], J1 = s_j1[i];
+        if (L.dom[0] && (J0 != cJ0 || J1 != cJ1)) {
+            c00 = P.ce.at(pw.i0, J0), c01 = P.ce.at(pw.i0, J1), c10 = P.ce.at(pw.i1, J0), c11 = P.ce.at(pw.i1, J1);
+            cJ0 = J0, cJ1 = J1;
+        }
+        const double ca = w0 * c00 + tt * c01, cb = w0 * c10 + tt * c11;
+        mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
+        step_f<U, (U & 1)>(sm, slot, L, G, w, A, k, pw, cN, ca, cb, px, mxp);
+        const int j = k - 3;
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<false>(P, L, j, lg, A, nullptr);
+        __syncwarp();
+        if (k + kRingW <= klast)
+            issue_row_w(sm, xin + int64_t(k + kRingW) * G.pitch + (a - 4), brow0 + int64_t(k + kRingW) * G.pitch,
+                        slot, bytes);
+        if (++slot == kRingW) slot = 0, phase ^= 1u;
+    };
+    for (int kb = kfirst; kb <= klast; kb += 4) {
+        row(std::integral_constant<int, 0>{}, kb);
+        if (kb + 1 <= klast) row(std::integral_constant<int, 1>{}, kb + 1);
+        if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, kb + 2);
+        if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, kb + 3);
+    }
+    fused_epilogue(P, A.mx, A.sx, A.cm, A.nan, mxp);
+}
+
+// kProlong -> kFused: the anchor of the prolonged field from the coarse correction,
+// sum(P ce) = sum ce(I, J) pax[I] pay[J], a fixed-order sum (blocks, then the last
+// block over the block partials by ticket). The field before the prolongation is
+// anchored (its mean is zero up to rounding), so c' = -sum(P ce) / cells.
+__global__ void __launch_bounds__(256) prolong_sum_kernel(Params P) {
+    Ctl* st = P.ctl;
+    if (!P.fuse || st->phase != kProlong || st->no_fuse) return;
+    __shared__ double red[8];
+    __shared__ int last;
+    const int ncx = P.ncx;
+    const int64_t n = int64_t(ncx) * P.ncy;
+    double v = 0.0;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int J = int(k / ncx), I = int(k - int64_t(J) * ncx);
+        v += (P.ce.at(I, J) * P.pax[I]) * P.pay[J];
+    }
+    v = warp_sum_down(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+        P.part[blockIdx.x] = s;
+        __threadfence();
+        last = atomicAdd(P.ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            double S = 0.0;
+            for (int b = 0; b < int(gridDim.x); ++b) S += __ldcg(&P.part[b]);
+            st->fshift = P.singular ? -(S / P.ncells) : -0.0;
+            st->phase = kFused;
+            *P.ticket = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // PH selects the phases a kernel serves: 0 all, 1 the sweep only, 2 the
 // prolongation / residual pass (prolong_w2). A single-GPU graph slot launches
 // PH 2 then PH 0; a multi-GPU slot PH 2, its exchange, PH 1, its exchange (the
@@ -896,8 +1224,9 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
 // 125 us per 4096^2 pass).
 template <bool MP, int PH>
 __global__ void __launch_bounds__(32, PH == 2 ? ISMG_FINE_MINB_PR
-                                              : (MP ? (PH == 1 ? ISMG_FINE_MINB_MP_SW : ISMG_FINE_MINB_MP)
-                                                    : ISMG_FINE_MINB))
+                                              : (PH == 3 ? ISMG_FINE_MINB_FU
+                                                         : (MP ? (PH == 1 ? ISMG_FINE_MINB_MP_SW : ISMG_FINE_MINB_MP)
+                                                               : ISMG_FINE_MINB)))
     fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
@@ -905,7 +1234,10 @@ __global__ void __launch_bounds__(32, PH == 2 ? ISMG_FINE_MINB_PR
     if (MP && threadIdx.x == 0 && (st.phase == kFine || st.phase == kProlong || st.phase == kResid))
         atomicMin(&P.ctl->mp_t0, (unsigned long long)gtimer());
 #endif
-    if (PH == 2) {
+    if (PH == 3) {
+        if constexpr (!MP)
+            if (st.phase == kFused) fused_w(sm, P, st, nq);
+    } else if (PH == 2) {
         if (st.phase == kProlong) prolong_w2<MP>(sm, P, st, nq, true);
         else if (st.phase == kResid) prolong_w2<MP>(sm, P, st, nq, false);
     } else if (PH == 1) {
@@ -946,6 +1278,13 @@ int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_o
         else if (ph2_only) fine_pass_w_kernel<true, 2><<<grid, 32, 0, st>>>(P, nq);
         else fine_pass_w_kernel<true, 1><<<grid, 32, 0, st>>>(P, nq);
         return 1;
+    }
+    if (P.fuse && !sweep_only && !ph2_only) {  // [anchor of P ce, PH 2 (rollback), fused pass, sweep]
+        prolong_sum_kernel<<<148, 256, 0, st>>>(P);
+        fine_pass_w_kernel<false, 2><<<grid, 32, 0, st>>>(P, nq);
+        fine_pass_w_kernel<false, 3><<<grid, 32, 0, st>>>(P, nq);
+        fine_pass_w_kernel<false, 0><<<grid, 32, 0, st>>>(P, nq);
+        return 4;
     }
     if (!sweep_only) fine_pass_w_kernel<false, 2><<<grid, 32, 0, st>>>(P, nq);
     if (ph2_only) return 1;

@@ -414,7 +414,8 @@ FusedEngine* make_fused(Solver& s) {
     const int nb = P.nstrips * P.nchunks;
     // per-CTA partials + per-32-CTA group partials; tickets: [all, per group, exchange (multi-GPU)]
     const int ngrp = (nb + 31) / 32;
-    ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * 3 * size_t(nb + ngrp)));
+    // (4 per CTA / group: the fused pass adds max |rp|; >= 148 for prolong_sum_kernel's partials)
+    ISMG_CUDA(cudaMalloc(&P.part, sizeof(double) * std::max<size_t>(148, 4 * size_t(nb + ngrp))));
     ISMG_CUDA(cudaMalloc(&P.ticket, sizeof(unsigned) * size_t(2 + ngrp)));
     ISMG_ZERO(P.ticket, sizeof(unsigned) * size_t(2 + ngrp));
     P.visit_cap = int(std::min<long long>(P.max_total + 2, 1 << 22));
@@ -434,6 +435,47 @@ FusedEngine* make_fused(Solver& s) {
     }
     ISMG_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
     plan_coarse(*e, L.h, c.device);
+    // the fused prolongation + sweep pass (fine_pass_w.cu fused_w): single GPU, one-warp
+    // strips, chunks of <= 96 rows, and uniform power-of-two tiles: every fine column /
+    // row extent a power of two and every column quad inside one coarse pair (what the
+    // pass's exact weight scaling assumes). ISMG_FUSE=0 turns it off (A/B hook).
+    {
+        const TileAxisH& ax = L.h.ax;
+        const TileAxisH& ay = L.h.ay;
+        auto pow2 = [](double d) {
+            uint64_t u;
+            std::memcpy(&u, &d, 8);
+            return d > 0.0 && (u & 0x000FFFFFFFFFFFFFull) == 0;
+        };
+        bool ok = e->fine_kind == 2 && !P.mp && P.H + 7 <= 104 && e->cond_state != 1;
+        if (const char* f = getenv("ISMG_FUSE")) ok = ok && f[0] != '0';
+        if (const char* g = getenv("ISMG_COND_GRAPH")) ok = ok && g[0] != '1';  // its SWITCH has no fused case
+        for (int i = 0; ok && i < P.nx; ++i) {
+            ok = pow2(ax.dk[size_t(i)]);
+            if (ok && (i & 3) != 0) ok = ax.k0[size_t(i)] == ax.k0[size_t(i - 1)] && ax.k1[size_t(i)] == ax.k1[size_t(i - 1)];
+        }
+        for (int j = 0; ok && j < P.ny; ++j) ok = pow2(ay.dk[size_t(j)]);
+        if (ok) {
+            // pax[I] = sum over fine columns i of the weight of coarse column I in P (the
+            // pass's ar = (dx - s) / dx on k0, sr = s / dx on k1); pay likewise
+            auto sums = [](const TileAxisH& a, int nc) {
+                std::vector<double> v(size_t(nc), 0.0);
+                for (int i = 0; i < a.n; ++i) {
+                    const double d = a.dk[size_t(i)], t = a.t[size_t(i)];
+                    v[size_t(a.k0[size_t(i)])] += (d - t) / d;
+                    v[size_t(a.k1[size_t(i)])] += t / d;
+                }
+                return v;
+            };
+            const std::vector<double> hx = sums(ax, L.h.ncx), hy = sums(ay, L.h.ncy);
+            double* d = nullptr;
+            ISMG_CUDA(cudaMalloc(&d, sizeof(double) * (hx.size() + hy.size())));
+            ISMG_H2D(d, hx.data(), sizeof(double) * hx.size());
+            ISMG_H2D(d + hx.size(), hy.data(), sizeof(double) * hy.size());
+            P.pax = d, P.pay = d + hx.size();
+            P.fuse = 1;
+        }
+    }
     (void)c;
     return e;
 }
@@ -445,6 +487,7 @@ void destroy_fused(FusedEngine* e) {
     if (e->cond_exec) cudaGraphExecDestroy(e->cond_exec);
     e->scratch.free();
     cudaFree(e->P.part);
+    if (e->P.pax) cudaFree(const_cast<double*>(e->P.pax));
     cudaFree(e->P.ticket);
     cudaFree(e->d_log);
     cudaFree(e->coarse_backup);
@@ -677,7 +720,7 @@ void fused_solve(Solver& s, Field& x, const Field& b, ismg_report& rep, Metrics&
     s.last.collectives = c.comm ? c.comm->collectives : 0;
     s.last.fine_pass_ms = 0.0;  // not separated on the fused path (coarse_ms is device-timed)
     s.last.kernel_launches = e.cond_state == 1 ? st.passes + st.coarse_launches * (e.cl_hybrid ? 2 : 1) + 2
-                                               : ((e.P.mp ? 3 : 2) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;
+                                               : ((e.P.mp ? 3 : 1 + e.fine_launches) + (e.cl_hybrid ? 1 : 0)) * launched_slots + 2;
 }
 
 }  // namespace ismgb

@@ -19,7 +19,10 @@ constexpr int kAheadRes = kRing - 2;    // rows prefetched ahead (prolong/residu
 constexpr int kCoarseThreads = 1024;
 constexpr int kCoarseSmemThreads = 512;
 
-enum Phase : int { kFine = 0, kCoarse = 1, kProlong = 2, kResid = 3, kDone = 4 };
+enum Phase : int { kFine = 0, kCoarse = 1, kProlong = 2, kResid = 3, kDone = 4, kFused = 5 };
+// kFused: the prolongation and the first sweep after it in ONE fine pass (single GPU,
+// uniform power-of-two tiles; fine_pass_w.cu fused_w); prolong_sum_kernel turns a
+// kProlong phase into kFused after computing the anchor of the prolonged field.
 
 // Device-resident solve state (one per solver).
 constexpr int kMaxRanks = 8;  // multi-GPU: ranks of one node
@@ -48,6 +51,8 @@ struct Ctl {
     int cl_hand, cl_hand_G;
     long long cl_hand_done;
     double cl_hand_rc;
+    double fshift;  // kFused: anchor shift of the prolonged field, -(sum of P ce) / cells
+    int no_fuse;    // the fused pass rolled back (its prolongation ended the solve): run PH 2 alone
 };
 
 struct Params {
@@ -91,6 +96,12 @@ struct Params {
     // the kernel that decides the next phase sets both conditions
     int cond;
     cudaGraphConditionalHandle h_while, h_switch;
+    // fused prolongation + sweep pass (single GPU, uniform power-of-two tiles):
+    // pax[I] / pay[J] = the prolongation weights of coarse column I / row J summed
+    // over the fine columns / rows, so sum(P ce) = sum ce(I, J) pax[I] pay[J]
+    int fuse;
+    const double* pax;
+    const double* pay;
 };
 
 // the next phase to the solve's conditional graph (no-op outside it). Built only
@@ -257,6 +268,7 @@ __device__ __forceinline__ void fine_decide_(const Params& P, int mode, double r
             s->phase = kFine;
         }
     } else if (mode == kProlong) {  // cycles.hpp:138-146
+        s->no_fuse = 0;
         s->prolongations += 1;
         if (r <= P.tol_fine) {
             s->phase = kDone, s->converged = 1;
@@ -273,6 +285,54 @@ __device__ __forceinline__ void fine_decide_(const Params& P, int mode, double r
         } else {
             to_coarse();
         }
+    }
+}
+
+// The fused pass (kFused): the prolongation's decision (cycles.hpp:138-146) on rp,
+// then the first sweep's (cycles.hpp:147-161) on r with prev = rp. Where the
+// prolongation itself ends the solve (rp <= tol, or the sweep budget is spent) the
+// pass's sweep must not count: roll back (buf[cur] still holds the input; PH 2
+// redoes the prolongation alone and decides).
+__device__ __forceinline__ void fine_decide_fused(const Params& P, double rp, double r, double sum, double rc0) {
+    Ctl* s = P.ctl;
+    s->passes += 1;
+    if (rp <= P.tol_fine || s->total >= P.max_total) {
+        s->no_fuse = 1;
+        s->phase = kProlong;
+        return;
+    }
+    s->prolongations += 1;
+    s->cur ^= 1;
+    s->prev = rp;
+    s->r = r;
+    if (P.singular) {
+        s->shift = -(sum / P.ncells);
+        s->has_shift = 1;
+    }
+    s->total += 1;
+    s->fine += 1;
+    if (s->nvisits > 0 && s->nvisits <= P.visit_cap) P.visit_log[2 * (s->nvisits - 1) + 1] += 1;
+    if (r <= P.tol_fine) {
+        s->phase = kDone, s->converged = 1;
+    } else if (s->total >= P.max_total) {
+        s->phase = kDone, s->converged = 0;
+    } else if (r > P.stall * s->prev) {
+        s->restrictions += 1;
+        if (s->nvisits < P.visit_cap) {
+            P.visit_log[2 * s->nvisits] = 0;
+            P.visit_log[2 * s->nvisits + 1] = 0;
+        }
+        s->nvisits += 1;
+        s->rc = rc0;
+        if (rc0 > P.tol_coarse) {
+            s->phase = kCoarse;
+        } else {
+            s->prev = r;
+            s->phase = kFine;
+        }
+    } else {
+        s->prev = r;
+        s->phase = kFine;
     }
 }
 
