@@ -1229,6 +1229,15 @@ __global__ void __launch_bounds__(32, PH == 2 ? ISMG_FINE_MINB_PR
                                                                : ISMG_FINE_MINB)))
     fine_pass_w_kernel(Params P, int nq) {
     __shared__ __align__(128) SmemW sm;
+    {  // not this kernel's phase: exit on one load (the snapshot below copies the whole Ctl
+       // through local memory; a no-op launch of 29k CTAs cost ~30 us with it, ncu launch list)
+        const int ph = *reinterpret_cast<const volatile int*>(&P.ctl->phase);
+        const bool mine = PH == 3   ? ph == kFused
+                          : PH == 2 ? (ph == kProlong || ph == kResid)
+                          : PH == 1 ? ph == kFine
+                                    : (ph == kFine || ph == kProlong || ph == kResid);
+        if (!mine) return;
+    }
     const Ctl st = *P.ctl;  // snapshot (written only by the previous kernel)
 #ifdef ISMG_MP_TRACE
     if (MP && threadIdx.x == 0 && (st.phase == kFine || st.phase == kProlong || st.phase == kResid))
