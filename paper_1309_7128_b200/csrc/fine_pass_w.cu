@@ -895,7 +895,10 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
 // sums run exactly as in sweep_w (cycles.hpp:148-152). The pass reads x, b and
 // writes x once: the two passes it replaces moved 48 B per cell, it moves 24.
 #ifndef ISMG_FINE_MINB_FU
-#define ISMG_FINE_MINB_FU 12
+// 11 resident warps (168 registers, no rematerialisation of the lane constants). Same-box
+// A/B (tools/visit_hist.py 16384 32 3, solve ms of steps 1-3): 11 -> 1239 / 1385 / 1880,
+// 12 (166 registers) -> 1308 / 1441 / 1943, 10 -> 1372 / 1495 / 2008 (profiles/r02_ab_fused_minb.txt)
+#define ISMG_FINE_MINB_FU 11
 #endif
 constexpr int kFuRows = 104;  // staged y-axis rows: chunk + 3 + 3 halo + 1
 
