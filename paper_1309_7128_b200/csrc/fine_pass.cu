@@ -430,7 +430,15 @@ __global__ void mp_unpack_kernel(Params P) {
         }
         const double* g = P.xch[0] + po;
         st->mp_seq = want;
-        fine_decide(P, int(__ldcv(g + 3)), m, sx, c);
+        const int mode = int(__ldcv(g + 3));
+        if (mode == kFused) {  // the fused pass: its prolongation residual too (pack scalar 5)
+            double rp = 0.0;
+            for (int r = 0; r < P.nranks; ++r) rp = fmax(rp, __ldcv(P.xch[r] + po + int64_t(r) * L + 5));
+            fine_decide_fused(P, rp, m, sx, c);
+            publish_phase(P, st->phase);
+        } else {
+            fine_decide(P, mode, m, sx, c);
+        }
 #ifdef ISMG_MP_TRACE
         const long long tu1 = gtimer();
         if (want % 64 == 0)

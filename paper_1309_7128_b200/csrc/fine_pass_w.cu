@@ -168,7 +168,8 @@ __device__ __forceinline__ double* my_pack(const Params& P, int p) {
 // the peers, followed by a system-scope release fence. Only the CTAs holding
 // the strip's first / last 3 rows push; tile sums and partials stay in the
 // local slot, where mp_unpack_kernel on every rank pulls them from.
-__device__ __forceinline__ void mp_push(const Params& P, const Lane& L, const Geo& G, int p, const double* xrows) {
+__device__ __forceinline__ void mp_push(const Params& P, const Lane& L, const Geo& G, int p, const double* xrows,
+                                        int hb = 0) {
     const int64_t o0 = (int64_t(p) * P.nranks + P.rank) * P.pack_len;
     bool pushed = false;
     for (int h = 0; h < 2; ++h) {
@@ -180,7 +181,7 @@ __device__ __forceinline__ void mp_push(const Params& P, const Lane& L, const Ge
             const double* src = xrows + int64_t(j) * P.pitch;
             const double2 v01 = *reinterpret_cast<const double2*>(src);
             const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
-            const int64_t off = o0 + P.h_off[h] + int64_t(j - hj) * P.pitch + kXOff + L.c0;
+            const int64_t off = o0 + P.h_off[hb + h] + int64_t(j - hj) * P.pitch + kXOff + L.c0;
             for (int q = 0; q < P.nranks; ++q) {
                 reinterpret_cast<double2*>(P.xch[q] + off)[0] = v01;
                 reinterpret_cast<double2*>(P.xch[q] + off)[1] = v23;
@@ -602,8 +603,9 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     const uint32_t bytes = uint32_t(((min(a + W + 4, P.nx + 5) - (a - 4)) + 1) & ~1) * 8u;
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
+    const bool alt = MP && st.no_fuse;  // redoing a fused pass's prolongation: the rows it read
     auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
-        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1) : xin + int64_t(k) * G.pitch + (a - 4);
+        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1, alt) : xin + int64_t(k) * G.pitch + (a - 4);
     };
     Acc A;
     // TileAxis::locate_cell of the lane's columns
@@ -1030,9 +1032,11 @@ __device__ __forceinline__ void step_f(const SmemW& sm, int slot, const Lane& L,
     for (int q = 0; q < 4; ++q) w.x[s0][q] = t[q];
 }
 
-// the fused pass's epilogue: warp_epilogue<false> with a fourth partial (max |rp|)
+// the fused pass's epilogue: warp_epilogue with a fourth partial (max |rp|); multi-GPU:
+// into this rank's pack slot (scalar 5) for mp_unpack_kernel, which decides
+template <bool MP>
 __device__ __forceinline__ void fused_epilogue(const Params& P, double mx, double sx, double cm, int nan,
-                                               double mp) {
+                                               double mp, const Ctl& st) {
     const int nb = gridDim.x * gridDim.y;
     const int bid = blockIdx.y * gridDim.x + blockIdx.x;
     const int lane = threadIdx.x & 31;
@@ -1084,13 +1088,22 @@ __device__ __forceinline__ void fused_epilogue(const Params& P, double mx, doubl
     c = warp_max(c);
     p = warp_max(p);
     if (lane == 0) {
-        fine_decide_fused(P, p, m, s, c);
-        publish_phase(P, P.ctl->phase);
+        if constexpr (MP) {
+            const int pp = int(st.mp_seq & 1ull);
+            double* mine = P.xch[P.rank] + (int64_t(pp) * P.nranks + P.rank) * P.pack_len;
+            mine[0] = m, mine[1] = c, mine[2] = 1.0, mine[3] = double(kFused), mine[4] = s, mine[5] = p;
+            fence_release_sys();
+            for (int q = 0; q < P.nranks; ++q) atomicExch(P.xflag[q] + P.rank, st.mp_seq + 1ull);
+        } else {
+            fine_decide_fused(P, p, m, s, c);
+            publish_phase(P, P.ctl->phase);
+        }
         *P.ticket = 0u;
         __threadfence();
     }
 }
 
+template <bool MP>
 __device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& st, int nq) {
     const int W = 4 * nq;
     const int a = blockIdx.x * W;
@@ -1107,6 +1120,11 @@ __device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& s
     const double* xin = st.buf[st.cur];
     const double* brow0 = st.b + (a - 4);
     const int kfirst = G.r0 - 3, klast = G.r1 + 2;
+    const int mpp = int(st.mp_seq & 1ull);  // multi-GPU: this pass's pack parity
+    double* mpk = MP ? my_pack(P, mpp) : nullptr;
+    auto xsrc = [&](int k) {  // x row k (multi-GPU: the neighbours' rows from the gathered packs)
+        return MP ? row_src(P, xin, k, a - 4, mpp ^ 1) : xin + int64_t(k) * G.pitch + (a - 4);
+    };
     // the lane's column weights and coarse pair (TileAxis::locate_cell of its columns)
     ProW pw;
     pw.i0 = pw.i1 = 0;
@@ -1136,8 +1154,7 @@ __device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& s
     }
     __syncwarp();
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
-        issue_row_w(sm, xin + int64_t(kfirst + s) * G.pitch + (a - 4), brow0 + int64_t(kfirst + s) * G.pitch, s,
-                    bytes);
+        issue_row_w(sm, xsrc(kfirst + s), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     Win w;
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -1163,11 +1180,9 @@ __device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& s
         mbar_wait_addr(bar0 + 8u * uint32_t(slot), phase);
         step_f<U, (U & 1)>(sm, slot, L, G, w, A, k, pw, cN, ca, cb, px, mxp);
         const int j = k - 3;
-        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<false>(P, L, j, lg, A, nullptr);
+        if (j >= G.r0 && j < G.r1 && ((j & tmask) == tmask || j == P.ny - 1)) tile_flush_w<MP>(P, L, j, lg, A, mpk);
         __syncwarp();
-        if (k + kRingW <= klast)
-            issue_row_w(sm, xin + int64_t(k + kRingW) * G.pitch + (a - 4), brow0 + int64_t(k + kRingW) * G.pitch,
-                        slot, bytes);
+        if (k + kRingW <= klast) issue_row_w(sm, xsrc(k + kRingW), brow0 + int64_t(k + kRingW) * G.pitch, slot, bytes);
         if (++slot == kRingW) slot = 0, phase ^= 1u;
     };
     for (int kb = kfirst; kb <= klast; kb += 4) {
@@ -1176,7 +1191,11 @@ __device__ __forceinline__ void fused_w(SmemW& sm, const Params& P, const Ctl& s
         if (kb + 2 <= klast) row(std::integral_constant<int, 2>{}, kb + 2);
         if (kb + 3 <= klast) row(std::integral_constant<int, 3>{}, kb + 3);
     }
-    fused_epilogue(P, A.mx, A.sx, A.cm, A.nan, mxp);
+    if (MP) {  // output rows for the next pass; input rows for a rollback's redo (h_off[2], [3])
+        mp_push(P, L, G, mpp, G.outp);
+        mp_push(P, L, G, mpp, xin + L.c0, 2);
+    }
+    fused_epilogue<MP>(P, A.mx, A.sx, A.cm, A.nan, mxp, st);
 }
 
 // kProlong -> kFused: the anchor of the prolonged field from the coarse correction,
@@ -1247,8 +1266,7 @@ __global__ void __launch_bounds__(32, PH == 2 ? ISMG_FINE_MINB_PR
         atomicMin(&P.ctl->mp_t0, (unsigned long long)gtimer());
 #endif
     if (PH == 3) {
-        if constexpr (!MP)
-            if (st.phase == kFused) fused_w(sm, P, st, nq);
+        if (st.phase == kFused) fused_w<MP>(sm, P, st, nq);
     } else if (PH == 2) {
         if (st.phase == kProlong) prolong_w2<MP>(sm, P, st, nq, true);
         else if (st.phase == kResid) prolong_w2<MP>(sm, P, st, nq, false);
@@ -1282,6 +1300,11 @@ void set_fine_pass_w_smem() {}
 dim3 fine_pass_w_grid(const Params& P) {
     const int W = 4 * fine_pass_w_quads(P.tile);
     return dim3((P.nx + W - 1) / W, P.nchunks);
+}
+// multi-GPU fused slot pieces (each followed by the caller's exchange where it moves data)
+void launch_prolong_sum(const Params& P, cudaStream_t st) { prolong_sum_kernel<<<148, 256, 0, st>>>(P); }
+void launch_fused_mp(const Params& P, dim3 grid, cudaStream_t st) {
+    fine_pass_w_kernel<true, 3><<<grid, 32, 0, st>>>(P, fine_pass_w_quads(P.tile));
 }
 int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only, bool ph2_only) {
     const int nq = fine_pass_w_quads(P.tile);

@@ -169,13 +169,19 @@ static cudaGraphExec_t graph_for(FusedEngine& e, int slots) {
     for (int k = 0; k < slots; ++k) {
         launch_coarse(e, e.P, c.stream);
         if (e.P.mp && e.fine_kind == 2 && !getenv("ISMG_MP_ALLPHASE")) {
-            // multi-GPU: [prolongation / residual pass, exchange, sweep pass, exchange]; the
-            // exchange after a pass that did not run (not its phase) returns at once
+            // multi-GPU: [(anchor of P ce,) prolongation / residual pass, exchange, (fused pass,
+            // exchange,) sweep pass, exchange]; the exchange after a pass that did not run (not
+            // its phase) returns at once
+            if (e.P.fuse) launch_prolong_sum(e.P, c.stream);
             launch_fine_pass_w(e.P, e.grid, c.stream, false, true);
             mp_exchange(e, c);
+            if (e.P.fuse) {
+                launch_fused_mp(e.P, e.grid, c.stream);
+                mp_exchange(e, c);
+            }
             launch_fine_pass_w(e.P, e.grid, c.stream, true, false);
             mp_exchange(e, c);
-            e.fine_launches = 3;  // (+1 exchange counted by the caller)
+            e.fine_launches = e.P.fuse ? 5 : 3;  // (+1 exchange counted by the caller)
             continue;
         }
         e.fine_launches = launch_fine(e, c.stream);
@@ -335,7 +341,7 @@ FusedEngine* make_fused(Solver& s) {
         for (auto& cr : e->coarse_rows) maxc = std::max(maxc, cr.second - cr.first);
         P.pack_cb_rows = maxc;
         const int64_t cbr = int64_t(maxc) * cpitch;
-        int64_t len = 8 + cbr + 6 * P.pitch;
+        int64_t len = 8 + cbr + 12 * P.pitch;  // + a fused pass's 3 + 3 input rows
         len = (len + 15) / 16 * 16;
         P.pack_len = int(len);
         P.rank = rank;
@@ -343,6 +349,7 @@ FusedEngine* make_fused(Solver& s) {
         const int cr0 = e->coarse_rows[size_t(rank)].first;
         P.cb_off = 8 - int64_t(cr0) * cpitch, P.cb_pitch = cpitch;
         P.h_off[0] = 8 + cbr, P.h_off[1] = 8 + cbr + 3 * P.pitch;
+        P.h_off[2] = 8 + cbr + 6 * P.pitch, P.h_off[3] = 8 + cbr + 9 * P.pitch;
         // exchange buffer [2][R][len] doubles + R flags, shared with the peers by CUDA IPC
         const size_t data = sizeof(double) * size_t(2) * size_t(R) * size_t(len);
         const size_t bytes = data + 256;
@@ -447,7 +454,8 @@ FusedEngine* make_fused(Solver& s) {
             std::memcpy(&u, &d, 8);
             return d > 0.0 && (u & 0x000FFFFFFFFFFFFFull) == 0;
         };
-        bool ok = e->fine_kind == 2 && !P.mp && P.H + 7 <= 104 && e->cond_state != 1;
+        bool ok = e->fine_kind == 2 && P.H + 7 <= 104 && e->cond_state != 1;
+        if (P.mp && getenv("ISMG_MP_ALLPHASE")) ok = false;  // that A/B path has no fused slot
         if (const char* f = getenv("ISMG_FUSE")) ok = ok && f[0] != '0';
         if (const char* g = getenv("ISMG_COND_GRAPH")) ok = ok && g[0] != '1';  // its SWITCH has no fused case
         for (int i = 0; ok && i < P.nx; ++i) {

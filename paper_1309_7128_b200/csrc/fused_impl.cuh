@@ -89,7 +89,7 @@ struct Params {
     double* xch[kMaxRanks];
     unsigned long long* xflag[kMaxRanks];
     int64_t cb_off, cb_pitch;  // pack offset of coarse cell (I, J): cb_off + J * cb_pitch + I
-    int64_t h_off[2];          // pack offsets of the first / last 3 rows
+    int64_t h_off[4];          // pack offsets of the first / last 3 rows; [2], [3]: a fused pass's INPUT rows (its rollback)
     View cbw;                  // single GPU: where the fused pass writes its tile sums (= cb)
     // conditional CUDA graph of the single-GPU solve (fused_host.cu): WHILE(phase
     // != done) { SWITCH(phase) { fine pass | coarse visit | prolong | resid } };
@@ -121,13 +121,16 @@ __device__ __forceinline__ void publish_phase(const Params& P, int phase) {
 
 // x-row source of the fused passes: the rank's own rows from the field, the
 // neighbours' rows from their packs of the previous pass (parity hp)
-__device__ __forceinline__ const double* row_src(const Params& P, const double* xin, int k, int col, int hp) {
-    if (P.mp) {
+__device__ __forceinline__ const double* row_src(const Params& P, const double* xin, int k, int col, int hp,
+                                                 bool alt = false) {
+    if (P.mp) {  // alt: the rows a fused pass read (its rollback redoes the prolongation on them)
         const double* x = P.xch[P.rank] + int64_t(hp) * P.nranks * P.pack_len;
         if (k < P.row0 && P.row0 > 0)
-            return x + int64_t(P.rank - 1) * P.pack_len + P.h_off[1] + int64_t(k - (P.row0 - 3)) * P.pitch + kXOff + col;
+            return x + int64_t(P.rank - 1) * P.pack_len + P.h_off[alt ? 3 : 1] + int64_t(k - (P.row0 - 3)) * P.pitch +
+                   kXOff + col;
         if (k >= P.row1 && P.row1 < P.ny)
-            return x + int64_t(P.rank + 1) * P.pack_len + P.h_off[0] + int64_t(k - P.row1) * P.pitch + kXOff + col;
+            return x + int64_t(P.rank + 1) * P.pack_len + P.h_off[alt ? 2 : 0] + int64_t(k - P.row1) * P.pitch + kXOff +
+                   col;
     }
     return xin + int64_t(k) * P.pitch + col;
 }
@@ -391,6 +394,8 @@ dim3 fine_pass_w_grid(const Params& P);
 int launch_fine_pass_w(const Params& P, dim3 grid, cudaStream_t st, bool sweep_only = false, bool ph2_only = false);
 void launch_finalize(const Params& P, View xuser, cudaStream_t st);
 void launch_mp_unpack(const Params& P, cudaStream_t st);
+void launch_prolong_sum(const Params& P, cudaStream_t st);
+void launch_fused_mp(const Params& P, dim3 grid, cudaStream_t st);
 void launch_coarse_global(const Params& P, cudaStream_t st);
 void launch_coarse_smem(const Params& P, double* backup, size_t smem, cudaStream_t st);
 void set_coarse_smem(size_t bytes);
