@@ -277,7 +277,10 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     double* rB = ringB + size_t(b) * kQB * 32 + lane;
     const uint32_t sE = su32(rE), sB = su32(rB);
     const uint32_t sN = su32(rN) + 8u * uint32_t(lane), sT = su32(tbl);  // this lane's ring column, class table
-    const bool has_n = b + 1 < T.nb, has_p = b > 0;
+    const bool has_n = b + 1 < T.nb;
+#ifdef ISMG_SP_INLINE_RES
+    const bool has_p = b > 0;
+#endif
     const double* xo_b = xo + size_t(b) * T.bstride + lane;
     const double* xo_n = (has_n ? xo + size_t(b + 1) * T.bstride : D.zero);  // row 32 (b+1) = next block's lane 0
     const double* bd_b = D.bd + size_t(b) * T.bstride + lane;
@@ -285,7 +288,9 @@ __device__ __forceinline__ void sp_sweep(const SpK& T, const SpD& D, SpShared& s
     // update: W (own previous output), S / SW (previous SE), N / NW (previous NE)
     double outP = 0.0, seP = 0.0, seP2 = 0.0, neP = 0.0, neP2 = 0.0;
     // residual window: rows r-1 (S*), r (W C E), r+1 (N*)
+#ifdef ISMG_SP_INLINE_RES
     double qSW = 0.0, qS = 0.0, qSE = 0.0, qW = 0.0, qC = 0.0, qE = 0.0, qNW = 0.0, qN = 0.0, qNE = 0.0;
+#endif
     double lmax = 0.0, rsum = 0.0;
     int avail = g == 0 ? kInf : 0;
     int h = 0;

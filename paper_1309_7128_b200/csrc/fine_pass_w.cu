@@ -655,7 +655,9 @@ __device__ __forceinline__ void prolong_w2(SmemW& sm, const Params& P, const Ctl
     for (int s = 0; s < kRingW && kfirst + s <= klast; ++s)
         issue_row_w(sm, xsrc(kfirst + s), brow0 + int64_t(kfirst + s) * G.pitch, s, bytes);
     const uint32_t bar0 = su32(&sm.bar[0]);
+#ifdef ISMG_PH2_ROLLED
     double x1[4] = {0, 0, 0, 0}, x2[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
+#endif
     int slot = 0;
     uint32_t phase = 0;
     const int si = 4 * L.l;
