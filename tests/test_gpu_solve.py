@@ -230,3 +230,56 @@ def test_coarse_register_wavefront_matches_oracle(dev, port, monkeypatch, case_n
     b.shift_interior(-b.interior_mean())
     solver.solve(x, b, RunMetrics(case.grid.nx * case.grid.ny))
     assert solver.last_stats()["coarse_engine"] == 4
+
+
+@pytest.mark.parametrize("case_name,nsteps", [("lid128t16", 6), ("jet64x128t16", 5)])
+def test_fused_prolongation_pass_matches_two_passes(dev, port, monkeypatch, case_name, nsteps):
+    """The fused prolongation + sweep pass (fine_pass_w.cu fused_w, uniform
+    power-of-two tiles) against the two-pass path (ISMG_FUSE=0) and the oracle:
+    identical per-step counts; fields equal to round-off (the fused pass takes the
+    prolonged field's anchor from a coarse-grid sum)."""
+    P = dev
+
+    def make():
+        if case_name.startswith("lid"):
+            case = setup_lid_cavity(128, 100.0)
+            case.dt = 100.0 / 128
+        else:
+            case = setup_jet(64, 128, 0.1, 16)
+        case.steps, case.t_max, case.steady_tol = nsteps, 0.0, 0.0
+        return case
+
+    cfg = CycleConfig(tile=16)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("ISMG_FUSE", fuse)
+        res = P.run_case(make(), cfg)
+        out[fuse] = res
+    case = make()
+    st = FluidState(case.grid)
+    st.dt, st.nu = case.dt, case.nu
+    rows, _ = port.run_steps(case.grid, cfg, st, nsteps)
+    want = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged) for r in rows]
+    assert sum(r.prolongations for r in rows) > 0  # the fused pass had work
+    for fuse, res in out.items():
+        got = [(r.fine_sweeps, r.coarse_sweeps, r.restrictions, r.prolongations, r.converged)
+               for r in res.metrics.rows]
+        assert got == want, fuse
+        for a, b in ((res.state.vel.u_data, st.vel.u_data), (res.state.vel.v_data, st.vel.v_data),
+                     (res.state.p.data, st.p.data)):
+            assert rel_l2(a, b) <= REL_L2, fuse
+    assert rel_l2(out["1"].state.p.data, out["0"].state.p.data) <= 1e-12
+    # the fused slot was planned: its graph slot launches two more kernels (anchor sum, fused pass)
+    grid = make().grid
+    rng = np.random.default_rng(5)
+    rhs = random_field(grid.nx, grid.ny, rng)
+    rhs.shift_interior(-rhs.interior_mean())
+    launches = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("ISMG_FUSE", fuse)
+        s = P.PressureSolver(grid, cfg)
+        rep = s.solve(ScalarField(grid.nx, grid.ny), rhs, RunMetrics(grid.nx * grid.ny))
+        st_ = s.last_stats()
+        launches[fuse] = (st_["kernel_launches"], rep.fine_sweeps, rep.coarse_sweeps, st_["prolong_passes"])
+    assert launches["1"][1:] == launches["0"][1:] and launches["1"][3] > 0
+    assert launches["1"][0] > launches["0"][0]
