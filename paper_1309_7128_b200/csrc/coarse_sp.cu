@@ -55,7 +55,10 @@ constexpr int kR = 3 + kD + kS;        // residual lag (steps): row 32's mirror 
 #else
 constexpr int kR = 0;                  // the residual is a pass over the sweep's output (no lag)
 #endif
-constexpr int kK = 5;                  // cp.async prefetch distance (steps)
+#ifndef ISMG_SP_K
+#define ISMG_SP_K 5
+#endif
+constexpr int kK = ISMG_SP_K;          // cp.async prefetch distance (steps)
 constexpr int kQ = 24;                 // new-value ring slots (3 segments of 8)
 constexpr int kQE = 8, kQB = 16;       // old-value / rhs ring slots
 constexpr int kEW = 33;                // old-value ring row: lanes 0..31 + row 32 (the next block's row 0, lane 31's NE)
